@@ -1,0 +1,152 @@
+/*
+ * b200map.h — C ABI of the B200-native Mapper-graph engine (libb200map.so).
+ *
+ * The reference (`nervemap`, /root/reference/pkg/src/nervemap) is pure
+ * Python with no FFI; each entry point below replaces one Python function of
+ * its hot path (cited file:line, relative to /root/reference/pkg/src/nervemap).
+ * INTEGRATION.md shows the ctypes binding a nervemap maintainer would add.
+ *
+ * Conventions
+ *   - Every pointer named d_* is DEVICE memory owned by the caller; h_* is
+ *     host memory owned by the caller.  The library never returns memory the
+ *     caller must free; internal scratch is stream-ordered and released
+ *     before the call returns.
+ *   - `stream` is a cudaStream_t (passed as void*); NULL = legacy stream.
+ *     Calls that must size outputs synchronise that stream.
+ *   - Return value: 0 on success, BM_ERR_DATA (-1) for invalid arguments
+ *     (maps to nervemap.errors.DataError), BM_ERR_INTERNAL (-2) for CUDA or
+ *     invariant failures (maps to InternalError), BM_ERR_NOMEM (-3) when a
+ *     device allocation fails.  The message is kept per calling thread and
+ *     read with bm_last_error().  No C++ exception crosses the ABI.
+ *   - Calls are re-entrant across host threads (each uses its own stream and
+ *     scratch), matching server.py's concurrent compute_mapper calls.
+ */
+#ifndef B200MAP_H
+#define B200MAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_OK 0
+#define BM_ERR_DATA (-1)
+#define BM_ERR_INTERNAL (-2)
+#define BM_ERR_NOMEM (-3)
+
+/* Exact fp64 summation order used for an element's distances
+ * (clustering.py:201-208 chooses it per element). */
+#define BM_ORDER_SEQUENTIAL 0 /* scipy cdist: s=0; s+=(x-y)^2 ... ; sqrt   (clustering.py:113,217) */
+#define BM_ORDER_PAIRWISE 1   /* numpy add.reduce pairwise tree; sqrt      (clustering.py:137-139) */
+
+/* Lens kinds (filters.py:14, 133-140) */
+#define BM_LENS_COLUMN 0
+#define BM_LENS_L2 1
+#define BM_LENS_LINF 2
+
+/* Distance engines for bm_cluster_elements (flags) */
+#define BM_ENGINE_AUTO 0  /* tensor-core candidates + exact recheck where supported */
+#define BM_ENGINE_EXACT 1 /* every pair evaluated in exact fp64 order on CUDA cores   */
+#define BM_ENGINE_TC 2    /* force the tcgen05 candidate engine                        */
+
+int bm_abi_version(void);
+const char* bm_last_error(void);
+/* Kernel launches issued by this library since load (benchmark evidence). */
+int64_t bm_launch_count(void);
+/* Number of visible CUDA devices (for the host-side GPU-count knob). */
+int bm_device_count(int* out);
+
+/* ---- K1: lens (filters.py:133-140, evaluate) --------------------------------
+ * out[i] = X[i,col]                         (BM_LENS_COLUMN, filters.py:135-136)
+ *        = sqrt(numpy_pairwise_sum(X[i]^2))  (BM_LENS_L2,    filters.py:137-138)
+ *        = max_j |X[i,j]|                    (BM_LENS_LINF,  filters.py:139-140)
+ * X is n x d row-major fp64. Bit-identical to numpy 2.x on x86-64. */
+int bm_lens_f64(int kind, const double* d_X, int64_t n, int64_t d, int64_t col,
+                double* d_out, void* stream);
+
+/* ---- normalize (dataset.py:165-186) ----------------------------------------
+ * scheme 1 = minmax, 2 = l2 (0 = none is a caller-side no-op). d_out may not
+ * alias d_X. Bit-identical to the numpy expressions in dataset.py:176-185. */
+int bm_normalize_f64(int scheme, const double* d_X, int64_t n, int64_t d,
+                     double* d_out, void* stream);
+
+/* ---- K2: cover binning (cover.py:122-140, membership) -----------------------
+ * f: n x m row-major fp64 filter values (m = 1 or 2).
+ * h_lo/h_hi: concatenated per-axis closed-interval endpoints
+ *            (axis 0 intervals first), exactly as cover._build_axis makes them.
+ * h_n_axis: intervals per axis (m entries). Elements are row-major over axes
+ *           (cover.py:56-61); n_el = prod(h_n_axis).
+ * Pass 1 writes h_counts[n_el] (rows per element; synchronises the stream).
+ * Pass 2 writes, for every element k, the ascending row ids of element k into
+ * d_rows[d_offsets[k] .. d_offsets[k+1]) where d_offsets (n_el+1, device) is
+ * the exclusive scan of the counts supplied by the caller. */
+int bm_membership_count(const double* d_f, int64_t n, int m, const double* h_lo,
+                        const double* h_hi, const int32_t* h_n_axis,
+                        int64_t* h_counts, void* stream);
+int bm_membership_fill(const double* d_f, int64_t n, int m, const double* h_lo,
+                       const double* h_hi, const int32_t* h_n_axis,
+                       const int64_t* d_offsets, int64_t* d_rows, void* stream);
+
+/* ---- K3..K6: per-element DBSCAN (clustering.py:151-198, 238-316) ------------
+ * X: n x d fp64 points. d_rows/h_offsets: memberships as produced above
+ * (element k owns d_rows[h_offsets[k] .. h_offsets[k+1])).
+ * h_order[k]: BM_ORDER_* for element k (clustering.py:201-208).
+ * Outputs:
+ *   d_labels[e]   cluster rank of membership entry e inside its element
+ *                 (clusters ordered by smallest row, clustering.py:192-197),
+ *                 or -1 for noise;
+ *   h_n_clusters[k] number of clusters of element k (synchronises the stream).
+ * engine: BM_ENGINE_*.  stats (optional, 8 int64): [0] pairs evaluated,
+ * [1] pairs rechecked in exact fp64, [2] tiles skipped, [3] tile pairs total,
+ * [4] adjacency bytes, [5] adjacency-stage device time (ns, CUDA events on
+ * `stream`), [6..7] reserved. */
+int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
+                        const int64_t* d_rows, const int64_t* h_offsets,
+                        int64_t n_el, double eps, int32_t min_pts,
+                        const uint8_t* h_order, int engine, int32_t* d_labels,
+                        int32_t* h_n_clusters, int64_t* h_stats, void* stream);
+
+/* Full n_rows x n_rows distance matrix of X[rows] in one exact order
+ * (clustering.py:96-113 pairwise_distances for BM_ORDER_SEQUENTIAL; the
+ * on-the-fly rows of clustering.py:137-139 for BM_ORDER_PAIRWISE).
+ * API helper for parity checks; the DBSCAN engine never materialises it. */
+int bm_pairwise_distances(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
+                          int64_t n_rows, int order, double* d_out, void* stream);
+
+/* ---- nodes (nerve.py:84-101): stable grouping of entries into node rows ----
+ * Given per-entry labels (above) and the per-element cluster counts, writes
+ * the rows of node v (dense ids in (element, cluster) order) into
+ * d_node_rows[d_node_offsets[v] .. d_node_offsets[v+1]) ascending, and
+ * d_node_offsets (n_nodes+1). n_nodes = sum(h_n_clusters). Returns the total
+ * number of clustered entries in *h_total. */
+int bm_group_nodes(const int64_t* d_rows, const int64_t* h_offsets, int64_t n_el,
+                   const int32_t* d_labels, const int32_t* h_n_clusters,
+                   int64_t* d_node_rows, int64_t* d_node_offsets,
+                   int64_t* h_total, void* stream);
+
+/* ---- K7: nerve edges (nerve.py:103-113) --------------------------------------
+ * Edges (s, t, w) with s < t, w = |rows_s ∩ rows_t| > 0, sorted
+ * lexicographically. The point-centric histogram yields exactly the
+ * overlapping_pairs candidates (cover.py:74-81) because a shared row implies
+ * overlapping elements. n_points bounds the row ids.
+ * Call with d_edges == NULL to get the count in *h_n_edges (synchronises);
+ * then again with d_edges (3 * n_edges int64, row-major s,t,w). */
+int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_offsets,
+                   int64_t n_nodes, int64_t n_points, int64_t* d_edges,
+                   int64_t* h_n_edges, void* stream);
+
+/* ---- node payload (nerve.py:60-62, 96) --------------------------------------
+ * d_stats[v*d + c] = numpy mean over node v's rows of column c (sequential
+ * row sum / size, as numpy's axis-0 mean); d_fmean[v*m + a] = numpy 1-D mean
+ * of the filter values (pairwise sum / size). */
+int bm_node_stats(const double* d_X, int64_t d, const double* d_f, int m,
+                  const int64_t* d_node_rows, const int64_t* d_node_offsets,
+                  int64_t n_nodes, double* d_stats, double* d_fmean,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200MAP_H */

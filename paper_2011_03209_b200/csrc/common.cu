@@ -1,0 +1,214 @@
+// common.cu — error state, scratch allocation and device-wide scans.
+#include <stdarg.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace bm {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+const char* get_error() { return g_err.c_str(); }
+
+int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
+  if (s.ptr) cudaFreeAsync(s.ptr, s.stream);
+  s.ptr = nullptr;
+  s.bytes = bytes;
+  s.stream = stream;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMallocAsync(&s.ptr, bytes, stream);
+  if (e != cudaSuccess) {
+    s.ptr = nullptr;
+    cudaGetLastError();
+    set_error("device scratch allocation of %zu bytes failed: %s", bytes,
+              cudaGetErrorString(e));
+    return BM_ERR_NOMEM;
+  }
+  return BM_OK;
+}
+
+int num_sms() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && cache[dev]) return cache[dev];
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (v <= 0) v = 148;
+  if (dev < 64) cache[dev] = v;
+  return v;
+}
+
+int make_pw_program(int64_t d, PwProgram* prog) {
+  std::vector<PwLeaf> leaves = pw_plan((int)d);
+  if ((int)leaves.size() > kMaxLeaves) {
+    set_error("dimension %lld too large for the pairwise program (max %d)",
+              (long long)d, kMaxLeaves * 128);
+    return BM_ERR_DATA;
+  }
+  prog->n_leaves = (int32_t)leaves.size();
+  int depth = 0, maxd = 0;
+  for (size_t i = 0; i < leaves.size(); ++i) {
+    prog->leaf[i] = leaves[i];
+    depth += 1;
+    if (depth > maxd) maxd = depth;
+    depth -= leaves[i].pops;
+  }
+  if (maxd > kMaxStack) {
+    set_error("pairwise program stack depth %d exceeds %d", maxd, kMaxStack);
+    return BM_ERR_DATA;
+  }
+  prog->depth = maxd;
+  return BM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan (int64), three phases. Chunk = 4096 elements per block.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = 8;
+constexpr int kScanChunk = kScanThreads * kScanPer;
+
+template <typename T>
+__device__ __forceinline__ int64_t load_as_i64(const T* p, int64_t i, int64_t n) {
+  return i < n ? (int64_t)p[i] : 0;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ int64_t block_exclusive_scan(int64_t v, int64_t* total) {
+  __shared__ int64_t warp_sums[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    int64_t w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int64_t warp_prefix = warp ? warp_sums[warp - 1] : 0;
+  *total = warp_sums[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+template <typename T>
+__global__ void scan_reduce_kernel(const T* in, int64_t n, int64_t* block_sums) {
+  int64_t base = (int64_t)blockIdx.x * kScanChunk;
+  int64_t s = 0;
+  for (int j = 0; j < kScanPer; ++j) s += load_as_i64(in, base + j * kScanThreads + threadIdx.x, n);
+  int64_t total;
+  block_exclusive_scan(s, &total);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void scan_blocksums_kernel(int64_t* sums, int64_t nb) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < nb ? sums[i] : 0;
+    int64_t total;
+    int64_t ex = block_exclusive_scan(v, &total);
+    if (i < nb) sums[i] = carry + ex;
+    carry += total;
+  }
+}
+
+template <typename T>
+__global__ void scan_apply_kernel(const T* in, int64_t* out, int64_t n,
+                                  const int64_t* block_sums) {
+  int64_t base = (int64_t)blockIdx.x * kScanChunk;
+  // blocked arrangement: thread t owns kScanPer consecutive items
+  int64_t v[kScanPer];
+  int64_t s = 0;
+  for (int j = 0; j < kScanPer; ++j) {
+    v[j] = load_as_i64(in, base + (int64_t)threadIdx.x * kScanPer + j, n);
+    s += v[j];
+  }
+  int64_t total;
+  int64_t ex = block_exclusive_scan(s, &total) + block_sums[blockIdx.x];
+  for (int j = 0; j < kScanPer; ++j) {
+    int64_t i = base + (int64_t)threadIdx.x * kScanPer + j;
+    if (i < n) out[i] = ex;
+    ex += v[j];
+  }
+}
+
+template <typename T>
+int exclusive_scan_impl(const T* d_in, int64_t* d_out, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return BM_OK;
+  int64_t nb = ceil_div(n, kScanChunk);
+  Scratch sums;
+  BM_TRY(scratch_alloc(sums, nb * sizeof(int64_t), stream));
+  scan_reduce_kernel<T><<<(unsigned)nb, kScanThreads, 0, stream>>>(d_in, n, sums.as<int64_t>());
+  BM_CHECK_LAUNCH();
+  scan_blocksums_kernel<<<1, 1024, 0, stream>>>(sums.as<int64_t>(), nb);
+  BM_CHECK_LAUNCH();
+  scan_apply_kernel<T><<<(unsigned)nb, kScanThreads, 0, stream>>>(d_in, d_out, n, sums.as<int64_t>());
+  BM_CHECK_LAUNCH();
+  return BM_OK;
+}
+
+}  // namespace
+
+int exclusive_scan_i64(const int64_t* d_in, int64_t* d_out, int64_t n, cudaStream_t stream) {
+  return exclusive_scan_impl<int64_t>(d_in, d_out, n, stream);
+}
+
+int exclusive_scan_i32_to_i64(const int32_t* d_in, int64_t* d_out, int64_t n,
+                              cudaStream_t stream) {
+  return exclusive_scan_impl<int32_t>(d_in, d_out, n, stream);
+}
+
+}  // namespace bm
+
+extern "C" {
+
+int bm_abi_version(void) { return 1; }
+
+int64_t bm_launch_count(void) { return bm::g_launches.load(); }
+
+const char* bm_last_error(void) { return bm::get_error(); }
+
+int bm_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (out) *out = n;
+  return BM_OK;
+}
+
+}  // extern "C"

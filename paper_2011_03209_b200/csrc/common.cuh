@@ -1,0 +1,148 @@
+// common.cuh — shared plumbing for libb200map: error state, scratch buffers,
+// device-wide scans, and the exact fp64 summation orders of the reference.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/b200map.h"
+
+namespace bm {
+
+// ---------------------------------------------------------------------------
+// Error plumbing: C++ never throws across the ABI; every entry point returns
+// a status and leaves a per-thread message.
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+const char* get_error();
+
+struct Status {
+  int code = BM_OK;
+};
+
+#define BM_CHECK_CUDA(expr)                                                   \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::bm::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr,            \
+                      cudaGetErrorString(_e));                                \
+      return _e == cudaErrorMemoryAllocation ? BM_ERR_NOMEM : BM_ERR_INTERNAL; \
+    }                                                                         \
+  } while (0)
+
+// Every kernel launch site ends with BM_CHECK_LAUNCH(), which also counts the
+// launch (bm_launch_count) so benchmarks can report how many of the
+// library's kernels ran.
+void count_launch();
+#define BM_CHECK_LAUNCH()       \
+  do {                          \
+    ::bm::count_launch();       \
+    BM_CHECK_CUDA(cudaGetLastError()); \
+  } while (0)
+
+#define BM_REQUIRE(cond, ...)        \
+  do {                               \
+    if (!(cond)) {                   \
+      ::bm::set_error(__VA_ARGS__);  \
+      return BM_ERR_DATA;            \
+    }                                \
+  } while (0)
+
+#define BM_TRY(expr)        \
+  do {                      \
+    int _rc = (expr);       \
+    if (_rc != BM_OK) return _rc; \
+  } while (0)
+
+// Stream-ordered scratch buffer released on scope exit (cudaFreeAsync).
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Number of SMs on the current device (cached per device).
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// Device-wide exclusive scan over int64 (in-place allowed). n may be 0.
+// ---------------------------------------------------------------------------
+int exclusive_scan_i64(const int64_t* d_in, int64_t* d_out, int64_t n,
+                       cudaStream_t stream);
+int exclusive_scan_i32_to_i64(const int32_t* d_in, int64_t* d_out, int64_t n,
+                              cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum; PW_BLOCKSIZE = 128) as a post-order program of leaves.
+// Leaf = contiguous run of <= 128 terms summed with 8 strided accumulators
+// (or sequentially from 0.0 when shorter than 8). After each leaf, `pops`
+// additions combine the top of the stack (left + right).
+// ---------------------------------------------------------------------------
+struct PwLeaf {
+  int32_t start;
+  int32_t len;
+  int32_t pops;  // number of stack reductions after pushing this leaf
+};
+
+inline void pw_plan_rec(int start, int n, std::vector<PwLeaf>& out) {
+  if (n <= 128) {
+    out.push_back({start, n, 0});
+    return;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_plan_rec(start, n2, out);
+  pw_plan_rec(start + n2, n - n2, out);
+  out.back().pops += 1;
+}
+
+inline std::vector<PwLeaf> pw_plan(int n) {
+  std::vector<PwLeaf> out;
+  if (n <= 0) return out;
+  pw_plan_rec(0, n, out);
+  return out;
+}
+
+constexpr int kMaxLeaves = 64;  // supports d <= 64*128 = 8192 dims
+constexpr int kMaxStack = 8;
+
+struct PwProgram {
+  int32_t n_leaves;
+  int32_t depth;  // max stack depth
+  PwLeaf leaf[kMaxLeaves];
+};
+
+int make_pw_program(int64_t d, PwProgram* prog);
+
+// Shift-register stack of partial sums in registers (static indexing only).
+struct PwStack {
+  double s[kMaxStack];
+  __device__ __forceinline__ void push(double v) {
+#pragma unroll
+    for (int i = kMaxStack - 1; i > 0; --i) s[i] = s[i - 1];
+    s[0] = v;
+  }
+  __device__ __forceinline__ void reduce() {
+    s[0] = __dadd_rn(s[1], s[0]);
+#pragma unroll
+    for (int i = 1; i < kMaxStack - 1; ++i) s[i] = s[i + 1];
+  }
+};
+
+}  // namespace bm

@@ -1,0 +1,736 @@
+// dbscan.cu — K3..K6: per-element DBSCAN over cover elements.
+//
+// Reference: nervemap/clustering.py:151-198 (dbscan), 201-208 (order
+// choice), 238-316 (cluster_all). Semantics reproduced exactly:
+//   count(i) = #{j : dist(i,j) <= eps}, self included          (:166)
+//   core     = count >= min_pts                                  (:167)
+//   clusters = connected components of core points under eps    (:169-182)
+//   border   = non-core with a core neighbour joins the cluster of its
+//              smallest-index core neighbour                     (:184-190)
+//   clusters ordered by smallest member (borders included)       (:192-197)
+// dist(i,j) is the fp64 value the reference computes for that element:
+// scipy cdist (sequential sum, no FMA) or numpy's pairwise row sum, then
+// sqrt, compared with eps AFTER the sqrt.
+//
+// Pipeline per batch of elements (see dbscan.cuh for the HBM layout):
+//   gather -> adjacency bitmap (exact fp64 tiles, or tcgen05 candidates +
+//   exact recheck, tc_engine.cu) -> counts -> core -> union-find over
+//   core-core bits (diagonal tiles first, then off-diagonal with global-root
+//   filtering) + border atomicMin -> canonical relabel.
+#include <algorithm>
+#include <vector>
+
+#include "dbscan.cuh"
+
+namespace bm {
+
+int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
+                       int64_t P, double eps, uint32_t* adj, const uint8_t* h_order,
+                       const std::vector<int32_t>& h_nrows, int64_t* stats,
+                       cudaStream_t stream);
+bool tc_supported(int64_t d);
+
+namespace {
+
+__constant__ PwProgram c_prog;
+
+// ---------------------------------------------------------------------------
+// gather: Xg[p] = X[rows[e]] (zero for pads). One warp per padded row.
+// ---------------------------------------------------------------------------
+__global__ void gather_kernel(const double* __restrict__ X, int64_t d,
+                              const int64_t* __restrict__ rows,
+                              const int64_t* __restrict__ offsets,  // n_el+1 (batch-relative)
+                              ElemTables et, int64_t P, double* __restrict__ Xg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
+       p += (int64_t)gridDim.x * wpb) {
+    int64_t a = 0, b = et.n_el;
+    while (b - a > 1) {
+      int64_t mid = (a + b) >> 1;
+      if (et.pbase[mid] <= p) a = mid; else b = mid;
+    }
+    int64_t i = p - et.pbase[a];
+    double* dst = Xg + p * d;
+    if (i < et.nrows[a]) {
+      const double* src = X + rows[offsets[a] + i] * d;
+      for (int64_t c = lane; c < d; c += 32) dst[c] = src[c];
+    } else {
+      for (int64_t c = lane; c < d; c += 32) dst[c] = 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp64 tile engine: every pair of a 128x128 tile in the reference's
+// exact order. 256 threads, 4x4 pairs per thread per 64x64 quadrant; the
+// rows of the current leaf (<=128 dims) are staged transposed in smem.
+// ---------------------------------------------------------------------------
+constexpr int kQ = 64;
+constexpr int kKC = 128;
+constexpr int kLd = kQ + 1;  // padded leading dimension (doubles)
+constexpr size_t kExactSmem = 2 * kKC * kLd * sizeof(double);
+
+struct Frag {
+  double v[16];
+};
+
+__device__ __forceinline__ void frag_zero(Frag& f, double z) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f.v[i] = z;
+}
+
+// f += (a - b)^2 for dim index `c` of the staged leaf (no FMA contraction)
+__device__ __forceinline__ void frag_step(Frag& f, const double* As, const double* Bs, int c,
+                                          int ty, int tx) {
+  double a[4], b[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = As[c * kLd + ty + 16 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = Bs[c * kLd + tx + 16 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double df = __dsub_rn(a[i], b[j]);
+      f.v[i * 4 + j] = __dadd_rn(f.v[i * 4 + j], __dmul_rn(df, df));
+    }
+}
+
+__device__ __forceinline__ void frag_first(Frag& f, const double* As, const double* Bs, int c,
+                                           int ty, int tx) {
+  double a[4], b[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = As[c * kLd + ty + 16 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = Bs[c * kLd + tx + 16 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double df = __dsub_rn(a[i], b[j]);
+      f.v[i * 4 + j] = __dmul_rn(df, df);
+    }
+}
+
+__device__ __forceinline__ void frag_add(Frag& a, const Frag& b) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a.v[i] = __dadd_rn(a.v[i], b.v[i]);
+}
+
+// accumulator j of a pairwise leaf: sequential over i = j, j+8, ... < body
+__device__ __forceinline__ void leaf_acc(Frag& f, const double* As, const double* Bs, int j,
+                                         int body, int ty, int tx) {
+  frag_first(f, As, Bs, j, ty, tx);
+  for (int i = j + 8; i < body; i += 8) frag_step(f, As, Bs, i, ty, tx);
+}
+
+// numpy pairwise_sum of one staged leaf of length len (loops_utils.h.src)
+__device__ __forceinline__ void leaf_pairwise(Frag& A, const double* As, const double* Bs,
+                                              int len, int ty, int tx) {
+  if (len < 8) {
+    frag_zero(A, -0.0);
+    for (int i = 0; i < len; ++i) frag_step(A, As, Bs, i, ty, tx);
+    return;
+  }
+  const int body = len - (len % 8);
+  Frag B, C, D;
+  leaf_acc(A, As, Bs, 0, body, ty, tx);
+  leaf_acc(B, As, Bs, 1, body, ty, tx);
+  frag_add(A, B);  // r0 + r1
+  leaf_acc(B, As, Bs, 2, body, ty, tx);
+  leaf_acc(C, As, Bs, 3, body, ty, tx);
+  frag_add(B, C);  // r2 + r3
+  frag_add(A, B);  // (r0+r1)+(r2+r3)
+  leaf_acc(B, As, Bs, 4, body, ty, tx);
+  leaf_acc(C, As, Bs, 5, body, ty, tx);
+  frag_add(B, C);
+  leaf_acc(C, As, Bs, 6, body, ty, tx);
+  leaf_acc(D, As, Bs, 7, body, ty, tx);
+  frag_add(C, D);
+  frag_add(B, C);  // (r4+r5)+(r6+r7)
+  frag_add(A, B);
+  for (int i = body; i < len; ++i) frag_step(A, As, Bs, i, ty, tx);
+}
+
+__device__ __forceinline__ void stage_rows(double* S, const double* __restrict__ Xg, int64_t d,
+                                           int64_t prow0, int nvalid, int c0, int len) {
+  const int total = kQ * len;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int r = idx / len, c = idx - r * len;
+    double v = 0.0;
+    if (r < nvalid) v = Xg[(prow0 + r) * d + c0 + c];
+    S[c * kLd + r] = v;
+  }
+}
+
+template <int DEPTH>
+__global__ void __launch_bounds__(256, 1)
+adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, double eps,
+                       uint32_t* __restrict__ adj, int64_t tile0) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + kKC * kLd;
+  __shared__ uint32_t bits[kTile * 4];
+
+  const int64_t g = tile0 + blockIdx.x;
+  int k, I, J;
+  decode_tile(et, g, k, I, J);
+  const int n_k = et.nrows[k];
+  const int64_t pb = et.pbase[k];
+  const int mode = et.order[k];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) bits[i] = 0u;
+
+  for (int q = 0; q < 4; ++q) {
+    const int qa = q >> 1, qb = q & 1;
+    const int ra = I * kTile + qa * kQ, rb = J * kTile + qb * kQ;  // local rows
+    if (ra >= n_k || rb >= n_k) continue;  // uniform
+    const int va = min(kQ, n_k - ra), vb = min(kQ, n_k - rb);
+    Frag acc;
+    Frag stk[DEPTH];
+    if (mode == BM_ORDER_SEQUENTIAL) {
+      frag_zero(acc, 0.0);
+      for (int c0 = 0; c0 < d; c0 += kKC) {
+        const int len = (int)((d - c0) < kKC ? (d - c0) : kKC);
+        __syncthreads();
+        stage_rows(As, Xg, d, pb + ra, va, c0, len);
+        stage_rows(Bs, Xg, d, pb + rb, vb, c0, len);
+        __syncthreads();
+        for (int c = 0; c < len; ++c) frag_step(acc, As, Bs, c, ty, tx);
+      }
+    } else {
+      for (int li = 0; li < c_prog.n_leaves; ++li) {
+        const PwLeaf lf = c_prog.leaf[li];
+        __syncthreads();
+        stage_rows(As, Xg, d, pb + ra, va, lf.start, lf.len);
+        stage_rows(Bs, Xg, d, pb + rb, vb, lf.start, lf.len);
+        __syncthreads();
+        Frag leaf;
+        leaf_pairwise(leaf, As, Bs, lf.len, ty, tx);
+        // push
+#pragma unroll
+        for (int s = DEPTH - 1; s > 0; --s) stk[s] = stk[s - 1];
+        stk[0] = leaf;
+        if constexpr (DEPTH > 1) {
+          for (int p = 0; p < lf.pops; ++p) {
+            frag_add(stk[1], stk[0]);
+#pragma unroll
+            for (int s = 0; s < DEPTH - 1; ++s) stk[s] = stk[s + 1];
+          }
+        }
+      }
+      acc = stk[0];
+    }
+    // decisions -> bit words (see header comment for the lane mapping)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int rl = ty + 16 * a;
+#pragma unroll
+      for (int bw = 0; bw < 2; ++bw) {
+        bool in0, in1;
+        {
+          const int cl = tx + 16 * (2 * bw);
+          double dist = __dsqrt_rn(__dadd_rn(0.0, acc.v[a * 4 + 2 * bw]));
+          in0 = rl < va && cl < vb && dist <= eps;
+        }
+        {
+          const int cl = tx + 16 * (2 * bw + 1);
+          double dist = __dsqrt_rn(__dadd_rn(0.0, acc.v[a * 4 + 2 * bw + 1]));
+          in1 = rl < va && cl < vb && dist <= eps;
+        }
+        unsigned m0 = __ballot_sync(0xffffffffu, in0);
+        unsigned m1 = __ballot_sync(0xffffffffu, in1);
+        const int R_even = qa * kQ + 2 * warp + 16 * a;
+        const int word = qb * 2 + bw;
+        if (lane == 0) bits[R_even * 4 + word] = (m0 & 0xffffu) | (m1 << 16);
+        if (lane == 16) bits[(R_even + 1) * 4 + word] = (m0 >> 16) | (m1 & 0xffff0000u);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* dst = adj + g * kTileWords;
+  for (int i = threadIdx.x; i < kTileWords; i += blockDim.x) dst[i] = bits[i];
+}
+
+// ---------------------------------------------------------------------------
+// counts from the bitmap: rows of every tile, columns of off-diagonal tiles
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+count_kernel(const uint32_t* __restrict__ adj, ElemTables et, int64_t n_tp,
+             int32_t* __restrict__ cnt) {
+  __shared__ uint32_t bits[kTileWords];
+  for (int64_t g = blockIdx.x; g < n_tp; g += gridDim.x) {
+    int k, I, J;
+    decode_tile(et, g, k, I, J);
+    const int64_t pb = et.pbase[k];
+    __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(adj + g * kTileWords);
+    uint4 w = src[threadIdx.x];
+    reinterpret_cast<uint4*>(bits)[threadIdx.x] = w;
+    int rc = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+    if (rc) atomicAdd(cnt + pb + I * kTile + threadIdx.x, rc);
+    if (I != J) {
+      __syncthreads();
+      const int c = threadIdx.x, wd = c >> 5, sh = c & 31;
+      int cc = 0;
+#pragma unroll 8
+      for (int r = 0; r < kTile; ++r) cc += (bits[r * 4 + wd] >> sh) & 1u;
+      if (cc) atomicAdd(cnt + pb + J * kTile + c, cc);
+    }
+  }
+}
+
+__global__ void core_init_kernel(const int32_t* __restrict__ cnt, ElemTables et, int64_t P,
+                                 int32_t min_pts, uint8_t* __restrict__ core,
+                                 int32_t* __restrict__ par, int32_t* __restrict__ bmin) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    core[p] = cnt[p] >= min_pts ? 1 : 0;  // pads have count 0 and min_pts >= 1
+    par[p] = (int32_t)p;
+    bmin[p] = kNoCore;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// union-find + border over the bitmap. DIAG selects the diagonal-tile pass
+// (run first) or the off-diagonal pass.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int lfind(int* lp, int x) {
+  while (true) {
+    int p = lp[x];
+    if (p == x) return x;
+    int gp = lp[p];
+    lp[x] = gp;
+    x = gp;
+  }
+}
+__device__ __forceinline__ bool lunion(int* lp, int a, int b) {
+  while (true) {
+    a = lfind(lp, a);
+    b = lfind(lp, b);
+    if (a == b) return false;
+    if (a > b) { int t = a; a = b; b = t; }
+    if (atomicCAS(lp + b, b, a) == b) return true;
+  }
+}
+
+template <bool DIAG>
+__global__ void __launch_bounds__(128)
+components_kernel(const uint32_t* __restrict__ adj, ElemTables et, int64_t n_tp,
+                  const uint8_t* __restrict__ core, int32_t* __restrict__ par,
+                  int32_t* __restrict__ bmin) {
+  __shared__ uint32_t bits[kTileWords];
+  __shared__ int groot[2 * kTile];  // global root of each tile node (-1: not core)
+  __shared__ int lp[2 * kTile];     // local union-find over tile nodes
+  __shared__ uint32_t coreJ[4], coreI[4];
+  __shared__ int any_merge;
+  const int t = threadIdx.x;
+  for (int64_t g = blockIdx.x; g < n_tp; g += gridDim.x) {
+    int k, I, J;
+    decode_tile(et, g, k, I, J);
+    if (DIAG != (I == J)) continue;  // uniform
+    const int64_t pb = et.pbase[k];
+    const int pI = (int)(pb + I * kTile), pJ = (int)(pb + J * kTile);
+    __syncthreads();
+    reinterpret_cast<uint4*>(bits)[t] = reinterpret_cast<const uint4*>(adj + g * kTileWords)[t];
+    const bool ci = core[pI + t], cj = core[pJ + t];
+    unsigned bi = __ballot_sync(0xffffffffu, ci), bj = __ballot_sync(0xffffffffu, cj);
+    if ((t & 31) == 0) { coreI[t >> 5] = bi; coreJ[t >> 5] = bj; }
+    groot[t] = ci ? uf_find(par, pI + t) : -1;
+    groot[kTile + t] = (!DIAG && cj) ? uf_find(par, pJ + t) : -1;
+    lp[t] = t;
+    lp[kTile + t] = kTile + t;
+    if (t == 0) any_merge = 0;
+    __syncthreads();
+    // --- core-core edges between nodes with different global roots
+    const int r = t;
+    if (ci) {
+      const int gr = groot[r];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
+        while (m) {
+          const int c = w * 32 + __ffs(m) - 1;
+          m &= m - 1;
+          const int node = DIAG ? c : kTile + c;
+          if (groot[node] != gr) {
+            if (lunion(lp, r, node)) any_merge = 1;
+          }
+        }
+      }
+    }
+    // --- border: non-core row r -> smallest core column
+    if (!ci && r < et.nrows[k] - I * kTile) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
+        if (m) {
+          const int c = w * 32 + __ffs(m) - 1;
+          const int cand = (DIAG ? pI : pJ) + c;
+          if (cand < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, cand);
+          break;
+        }
+      }
+    }
+    // --- border: non-core column c -> smallest core row (off-diagonal only)
+    if (!DIAG && !cj && t < et.nrows[k] - J * kTile) {
+      const int c = t, wd = c >> 5, sh = c & 31;
+      for (int rr = 0; rr < kTile; ++rr) {
+        if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u)) {
+          const int cand = pI + rr;
+          if (cand < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, cand);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    // --- propagate local merges to the global forest
+    if (any_merge) {
+      for (int x = t; x < 2 * kTile; x += blockDim.x) {
+        if (groot[x] < 0) continue;
+        const int lr = lfind(lp, x);
+        if (lr != x && groot[lr] != groot[x]) uf_union(par, groot[x], groot[lr]);
+      }
+    }
+  }
+}
+
+__global__ void compress_kernel(int32_t* __restrict__ par, const uint8_t* __restrict__ core,
+                                int64_t P) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (core[p]) par[p] = uf_find(par, (int)p);
+}
+
+// root label per padded index (-1 noise), and cluster min member via atomicMin
+__global__ void label_kernel(ElemTables et, int64_t P, const uint8_t* __restrict__ core,
+                             int32_t* __restrict__ par, const int32_t* __restrict__ bmin,
+                             int32_t* __restrict__ lab, int32_t* __restrict__ cmin) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int root = -1;
+    if (core[p]) root = uf_find(par, (int)p);
+    else if (bmin[p] != kNoCore) root = uf_find(par, bmin[p]);
+    lab[p] = root;
+    if (root >= 0) atomicMin(cmin + root, (int)p);
+  }
+}
+
+__global__ void head_kernel(int64_t P, const int32_t* __restrict__ lab,
+                            const int32_t* __restrict__ cmin, int32_t* __restrict__ head) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int r = lab[p];
+    head[p] = (r >= 0 && cmin[r] == (int)p) ? 1 : 0;
+  }
+}
+
+__global__ void output_kernel(ElemTables et, const int64_t* __restrict__ offsets,
+                              int64_t n_entries, const int32_t* __restrict__ lab,
+                              const int32_t* __restrict__ cmin,
+                              const int64_t* __restrict__ hscan, int32_t* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = et.n_el;
+    while (b - a > 1) {
+      int64_t mid = (a + b) >> 1;
+      if (offsets[mid] <= e) a = mid; else b = mid;
+    }
+    // skip empty elements sharing the same offset: the owning element is the
+    // last one whose offset <= e and that has rows (offsets strictly increase
+    // across non-empty elements)
+    const int64_t p = et.pbase[a] + (e - offsets[a]);
+    const int r = lab[p];
+    out[e] = r >= 0 ? (int32_t)(hscan[cmin[r]] - hscan[et.pbase[a]]) : -1;
+  }
+}
+
+__global__ void fill_total_kernel(int64_t* hs, const int32_t* hd, int64_t P) {
+  hs[P] = (P > 0 ? hs[P - 1] + hd[P - 1] : 0);
+}
+
+__global__ void nclusters_kernel(ElemTables et, const int64_t* __restrict__ hscan,
+                                 int32_t* __restrict__ ncl) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < et.n_el) ncl[k] = (int32_t)(hscan[et.pbase[k + 1]] - hscan[et.pbase[k]]);
+}
+
+inline unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
+  int64_t b = ceil_div(n, threads);
+  int64_t cap = (int64_t)num_sms() * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+template <int DEPTH>
+int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, double eps,
+                       uint32_t* adj, cudaStream_t stream) {
+  static bool attr_done = false;  // per process; attribute is per function
+  if (!attr_done) {
+    BM_CHECK_CUDA(cudaFuncSetAttribute(adjacency_exact_kernel<DEPTH>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kExactSmem));
+    attr_done = true;
+  }
+  const int64_t kMaxGrid = 1ll << 30;
+  for (int64_t t0 = 0; t0 < n_tp; t0 += kMaxGrid) {
+    int64_t nb = std::min<int64_t>(kMaxGrid, n_tp - t0);
+    adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(Xg, d, et, eps, adj,
+                                                                            t0);
+    BM_CHECK_LAUNCH();
+  }
+  return BM_OK;
+}
+
+int exact_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
+                          double eps, uint32_t* adj, cudaStream_t stream) {
+  PwProgram prog;
+  BM_TRY(make_pw_program(d, &prog));
+  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
+                                        stream));
+  switch (prog.depth) {
+    case 1: return launch_exact_depth<1>(Xg, d, et, n_tp, eps, adj, stream);
+    case 2: return launch_exact_depth<2>(Xg, d, et, n_tp, eps, adj, stream);
+    case 3: return launch_exact_depth<3>(Xg, d, et, n_tp, eps, adj, stream);
+    case 4: return launch_exact_depth<4>(Xg, d, et, n_tp, eps, adj, stream);
+    default: return launch_exact_depth<kMaxStack>(Xg, d, et, n_tp, eps, adj, stream);
+  }
+}
+
+// full distance matrix of a row subset in one exact order (API helper)
+__global__ void pairwise_matrix_kernel(const double* __restrict__ X, int64_t d,
+                                       const int64_t* __restrict__ rows, int64_t n, int order,
+                                       double* __restrict__ out) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n, j = idx - i * n;
+    const double s = exact_dist2(X + rows[i] * d, X + rows[j] * d, d, order, c_prog);
+    out[idx] = __dsqrt_rn(s);
+  }
+}
+
+// host-side batch description
+struct Batch {
+  int64_t k0, k1;  // element range [k0, k1)
+};
+
+}  // namespace
+
+// Exposed for the tcgen05 engine's verification path.
+int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, double eps,
+                        uint32_t* adj, cudaStream_t stream) {
+  return exact_build_adjacency(Xg, d, et, n_tp, eps, adj, stream);
+}
+
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
+                                   const int64_t* d_rows, const int64_t* h_offsets,
+                                   int64_t n_el, double eps, int32_t min_pts,
+                                   const uint8_t* h_order, int engine, int32_t* d_labels,
+                                   int32_t* h_n_clusters, int64_t* h_stats, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  BM_REQUIRE(n >= 0 && d >= 1 && n_el >= 0, "bad shapes");
+  BM_REQUIRE(eps > 0.0, "eps must be positive");
+  BM_REQUIRE(min_pts >= 1, "min-pts must be >= 1");
+  BM_REQUIRE(h_offsets && h_n_clusters && h_order, "null host table");
+  BM_REQUIRE(engine == BM_ENGINE_AUTO || engine == BM_ENGINE_EXACT || engine == BM_ENGINE_TC,
+             "unknown engine %d", engine);
+  int64_t stats_local[8] = {0};
+  int64_t* stats = h_stats ? h_stats : stats_local;
+  for (int i = 0; i < 8; ++i) stats[i] = 0;
+  for (int64_t k = 0; k < n_el; ++k) h_n_clusters[k] = 0;
+  if (n_el == 0) return BM_OK;
+  for (int64_t k = 0; k < n_el; ++k) {
+    BM_REQUIRE(h_offsets[k + 1] >= h_offsets[k], "offsets must be non-decreasing");
+    BM_REQUIRE(h_order[k] == BM_ORDER_SEQUENTIAL || h_order[k] == BM_ORDER_PAIRWISE,
+               "bad order flag");
+  }
+  if (h_offsets[n_el] == h_offsets[0]) return BM_OK;
+  BM_REQUIRE(d_X && d_rows && d_labels, "null device pointer");
+  PwProgram probe;
+  BM_TRY(make_pw_program(d, &probe));
+
+  bool use_tc = false;
+  if (engine == BM_ENGINE_TC) {
+    BM_REQUIRE(tc_supported(d), "tensor-core engine does not support d=%lld", (long long)d);
+    use_tc = true;
+  } else if (engine == BM_ENGINE_AUTO) {
+    use_tc = tc_supported(d);
+  }
+
+  // ---- batches bounded by the adjacency budget (bytes)
+  size_t free_b = 0, total_b = 0;
+  BM_CHECK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = 0.55 * (double)free_b;
+  std::vector<Batch> batches;
+  {
+    int64_t k0 = 0;
+    double acc = 0;
+    for (int64_t k = 0; k < n_el; ++k) {
+      int64_t nk = h_offsets[k + 1] - h_offsets[k];
+      int64_t T = ceil_div(nk, kTile);
+      double bytes = (double)(T * (T + 1) / 2) * kTileWords * 4 +
+                     (double)T * kTile * (d * 8.0 + 4 * 4 + 1 + d * 2.0);
+      BM_REQUIRE(T * kTile < (1ll << 31), "element %lld too large", (long long)k);
+      if (bytes > budget) {
+        set_error("element %lld (%lld rows) needs %.1f GB of adjacency; exceeds device budget "
+                  "%.1f GB (row-block sharding over several GPUs required)",
+                  (long long)k, (long long)nk, bytes / 1e9, budget / 1e9);
+        return BM_ERR_NOMEM;
+      }
+      if (acc + bytes > budget && k > k0) {
+        batches.push_back({k0, k});
+        k0 = k;
+        acc = 0;
+      }
+      acc += bytes;
+    }
+    batches.push_back({k0, n_el});
+  }
+
+  for (const Batch& bt : batches) {
+    const int64_t nb_el = bt.k1 - bt.k0;
+    std::vector<int64_t> tp_off(nb_el + 1, 0), offs(nb_el + 1, 0);
+    std::vector<int32_t> pbase(nb_el + 1, 0), nrows(nb_el), ntiles(nb_el);
+    std::vector<uint8_t> order(nb_el);
+    for (int64_t i = 0; i < nb_el; ++i) {
+      int64_t k = bt.k0 + i;
+      int64_t nk = h_offsets[k + 1] - h_offsets[k];
+      int64_t T = ceil_div(nk, kTile);
+      nrows[i] = (int32_t)nk;
+      ntiles[i] = (int32_t)T;
+      order[i] = h_order[k];
+      tp_off[i + 1] = tp_off[i] + T * (T + 1) / 2;
+      pbase[i + 1] = (int32_t)(pbase[i] + T * kTile);
+      offs[i] = h_offsets[k] - h_offsets[bt.k0];
+    }
+    offs[nb_el] = h_offsets[bt.k1] - h_offsets[bt.k0];
+    const int64_t n_tp = tp_off[nb_el];
+    const int64_t P = pbase[nb_el];
+    const int64_t n_entries = offs[nb_el];
+    if (n_entries == 0) continue;
+
+    // ---- device tables
+    Scratch tabs;
+    size_t tab_bytes = (nb_el + 1) * 8 * 2 + (nb_el + 1) * 4 * 3 + nb_el + 64;
+    BM_TRY(scratch_alloc(tabs, tab_bytes, stream));
+    char* tp = tabs.as<char>();
+    int64_t* d_tp_off = (int64_t*)tp;
+    int64_t* d_offs = d_tp_off + nb_el + 1;
+    int32_t* d_pbase = (int32_t*)(d_offs + nb_el + 1);
+    int32_t* d_nrows = d_pbase + nb_el + 1;
+    int32_t* d_ntiles = d_nrows + nb_el + 1;
+    uint8_t* d_order = (uint8_t*)(d_ntiles + nb_el + 1);
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_tp_off, tp_off.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_offs, offs.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_pbase, pbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_nrows, nrows.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_ntiles, ntiles.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_order, order.data(), nb_el, cudaMemcpyHostToDevice, stream));
+    ElemTables et{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, nb_el};
+
+    // ---- gather rows (fp64, membership order, padded)
+    Scratch xg;
+    BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
+    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(
+        d_X, d, d_rows + h_offsets[bt.k0], d_offs, et, P, xg.as<double>());
+    BM_CHECK_LAUNCH();
+
+    // ---- adjacency bitmap
+    Scratch adj;
+    BM_TRY(scratch_alloc(adj, (size_t)n_tp * kTileWords * 4, stream));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    BM_CHECK_CUDA(cudaEventCreate(&ev0));
+    BM_CHECK_CUDA(cudaEventCreate(&ev1));
+    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+    if (use_tc) {
+      BM_TRY(tc_build_adjacency(xg.as<double>(), d, et, n_tp, P, eps, adj.as<uint32_t>(),
+                                order.data(), nrows, stats, stream));
+    } else {
+      BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, n_tp, eps, adj.as<uint32_t>(),
+                                   stream));
+      for (int64_t i = 0; i < nb_el; ++i) stats[0] += (int64_t)nrows[i] * (nrows[i] + 1) / 2;
+    }
+    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+    stats[3] += n_tp;
+    stats[4] = std::max<int64_t>(stats[4], n_tp * kTileWords * 4);
+
+    // ---- counts, core, union-find, border
+    Scratch work;
+    size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
+    BM_TRY(scratch_alloc(work, wbytes, stream));
+    int32_t* cnt = work.as<int32_t>();
+    int32_t* par = cnt + P;
+    int32_t* bmin = par + P;
+    int32_t* lab = bmin + P;
+    int32_t* cmin = lab + P;
+    int32_t* head = cmin + P;
+    int64_t* hscan = (int64_t*)(((uintptr_t)(head + P) + 15) & ~(uintptr_t)15);
+    uint8_t* core = (uint8_t*)(hscan + P + 1);
+    BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
+    const unsigned tgrid = grid_for(n_tp, 1, 32);
+    count_kernel<<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, cnt);
+    BM_CHECK_LAUNCH();
+    core_init_kernel<<<grid_for(P, 256), 256, 0, stream>>>(cnt, et, P, min_pts, core, par, bmin);
+    BM_CHECK_LAUNCH();
+    components_kernel<true><<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, core, par,
+                                                       bmin);
+    BM_CHECK_LAUNCH();
+    compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par, core, P);
+    BM_CHECK_LAUNCH();
+    components_kernel<false><<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, core, par,
+                                                        bmin);
+    BM_CHECK_LAUNCH();
+    label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par, bmin, lab, cmin);
+    BM_CHECK_LAUNCH();
+    head_kernel<<<grid_for(P, 256), 256, 0, stream>>>(P, lab, cmin, head);
+    BM_CHECK_LAUNCH();
+    BM_TRY(exclusive_scan_i32_to_i64(head, hscan, P, stream));
+    fill_total_kernel<<<1, 1, 0, stream>>>(hscan, head, P);  // hscan[P] = #heads
+    BM_CHECK_LAUNCH();
+    Scratch ncl_d;
+    BM_TRY(scratch_alloc(ncl_d, nb_el * 4, stream));
+    nclusters_kernel<<<(unsigned)ceil_div(nb_el, 128), 128, 0, stream>>>(et, hscan,
+                                                                          ncl_d.as<int32_t>());
+    BM_CHECK_LAUNCH();
+    output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(
+        et, d_offs, n_entries, lab, cmin, hscan, d_labels + h_offsets[bt.k0]);
+    BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaMemcpyAsync(h_n_clusters + bt.k0, ncl_d.ptr, nb_el * 4,
+                                  cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    float ms = 0.f;
+    BM_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats[5] += (int64_t)(ms * 1e6);  // adjacency (distance) stage, ns on the launch stream
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
+  return BM_OK;
+}
+
+
+extern "C" int bm_pairwise_distances(const double* d_X, int64_t n, int64_t d,
+                                     const int64_t* d_rows, int64_t n_rows, int order,
+                                     double* d_out, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  BM_REQUIRE(n >= 0 && d >= 1 && n_rows >= 0, "bad shapes");
+  BM_REQUIRE(order == BM_ORDER_SEQUENTIAL || order == BM_ORDER_PAIRWISE, "bad order");
+  if (n_rows == 0) return BM_OK;
+  BM_REQUIRE(d_X && d_rows && d_out, "null pointer");
+  PwProgram prog;
+  BM_TRY(make_pw_program(d, &prog));
+  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
+                                        stream));
+  pairwise_matrix_kernel<<<grid_for(n_rows * n_rows, 128, 32), 128, 0, stream>>>(
+      d_X, d, d_rows, n_rows, order, d_out);
+  BM_CHECK_LAUNCH();
+  return BM_OK;
+}

@@ -1,0 +1,125 @@
+"""GPU parity of K3..K6 (per-element DBSCAN) — mirrors the reference's
+test_clustering.py cases and checks randomized instances against the oracle,
+in both exact fp64 orders and on every engine."""
+
+import numpy as np
+import pytest
+
+from oracle import mapper_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = [1, 0]  # exact, auto (tensor-core candidates where supported)
+
+
+def run(pts, rows, eps, min_pts, order=0, engine=0):
+    from paper_2011_03209_b200 import DbscanParams, from_array
+    from paper_2011_03209_b200.clustering import dbscan_rows
+
+    pc = from_array(np.asarray(pts, dtype=np.float64))
+    return dbscan_rows(pc, rows, DbscanParams(eps, min_pts), order=order, engine=engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_two_far_pairs(engine):  # test_clustering.py:71-75
+    out = run([0.0, 0.1, 5.0, 5.1], np.arange(4), 0.2, 2, engine=engine)
+    assert out.clusters == [[0, 1], [2, 3]] and out.noise == []
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_all_noise(engine):
+    out = run([0.0, 10.0], np.arange(2), 1.0, 2, engine=engine)
+    assert out.clusters == [] and out.noise == [0, 1]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_eps_inclusive_and_self_counted(engine):
+    out = run([0.0, 1.0], np.arange(2), 1.0, 2, engine=engine)
+    assert out.clusters == [[0, 1]]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_border_smallest_core_neighbor(engine):
+    pts = [0.0, 0.4, 0.7, 1.0, 2.0, 3.0, 3.3, 3.6, 4.0]
+    out = run(pts, np.arange(9), 1.0, 4, engine=engine)
+    assert out.clusters == [[0, 1, 2, 3, 4], [5, 6, 7, 8]]
+
+
+def test_global_row_ids_preserved():
+    pts = np.zeros((31, 1))
+    rows = np.array([10, 11, 20, 21, 30])
+    pts[rows, 0] = [0.0, 0.1, 9.0, 9.1, 50.0]
+    out = run(pts, rows, 0.5, 2, order=1)
+    assert out.clusters == [[10, 11], [20, 21]] and out.noise == [30]
+
+
+@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("engine", ENGINES)
+def test_randomized_against_oracle(seed, engine):
+    rng = np.random.default_rng(7_000 + seed)
+    n = int(rng.integers(1, 700))
+    d = int(rng.integers(1, 70))
+    pts = rng.uniform(0.0, 4.0, (n, d)) if seed % 2 else \
+        O.gmm(n, d, int(rng.integers(1, 5)), 3.0, seed)
+    eps = O.dist_quantile(pts, float(rng.uniform(0.02, 0.4)), seed)
+    min_pts = int(rng.integers(1, 9))
+    rows = np.arange(n)
+    for order in (O.ORDER_SEQUENTIAL, O.ORDER_PAIRWISE):
+        out = run(pts, rows, eps, min_pts, order=order, engine=engine)
+        clusters, noise = O.dbscan_element(pts, rows, eps, min_pts, order)
+        assert out.clusters == clusters, f"seed={seed} order={order}"
+        assert out.noise == noise
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_tile_boundaries_and_many_elements(engine):
+    """Elements straddling the 128-row tile size, several per launch."""
+    from paper_2011_03209_b200 import DbscanParams, DistanceStrategy, cluster_all, from_array
+
+    rng = np.random.default_rng(3)
+    X = O.gmm(3000, 12, 4, 4.0, 3)
+    pc = from_array(X)
+    sizes = [1, 2, 127, 128, 129, 255, 256, 257, 0, 600, 1000]
+    members = [np.sort(rng.choice(3000, s, replace=False)) for s in sizes]
+    eps = O.dist_quantile(X, 0.1)
+    strategy = DistanceStrategy(threshold=200)
+    out = cluster_all(pc, members, DbscanParams(eps, 4), strategy, engine=engine)
+    for k, rows in enumerate(members):
+        order = O.element_order(len(rows), "precomputed", 200)
+        clusters, noise = O.dbscan_element(X, rows, eps, 4, order)
+        assert out[k].element_index == k
+        assert out[k].clusters == clusters, k
+        assert out[k].noise == noise
+
+
+def test_exact_ties_follow_the_element_order():
+    """The 256-D tie: cdist and numpy disagree; each order reproduces its mode."""
+    import cases
+
+    X, params = cases.tie_case()
+    eps = params["eps"]
+    rows = np.arange(len(X))
+    pre = run(X, rows, eps, 2, order=O.ORDER_SEQUENTIAL)
+    fly = run(X, rows, eps, 2, order=O.ORDER_PAIRWISE)
+    assert (pre.clusters, pre.noise) == O.dbscan_element(X, rows, eps, 2, O.ORDER_SEQUENTIAL)
+    assert (fly.clusters, fly.noise) == O.dbscan_element(X, rows, eps, 2, O.ORDER_PAIRWISE)
+    assert pre.clusters != fly.clusters
+
+
+def test_cancel_check_is_polled():
+    from paper_2011_03209_b200 import DbscanParams, DistanceStrategy, cluster_all, from_array
+
+    class Stop(Exception):
+        pass
+
+    calls = []
+
+    def cancel():
+        calls.append(1)
+        raise Stop()
+
+    pc = from_array(np.random.default_rng(0).standard_normal((50, 2)))
+    with pytest.raises(Stop):
+        cluster_all(pc, [np.arange(50)], DbscanParams(0.5, 3), DistanceStrategy(),
+                    cancel_check=cancel)
+    assert calls

@@ -166,6 +166,7 @@ def cluster_device(X, rows_dev, offsets, params: DbscanParams, orders, cancel_ch
         ncl[k0:k1] = nc
         stats[:4] += st[:4]
         stats[4] = max(stats[4], st[4])
+        stats[5:] += st[5:]
     return labels[: int(offsets[-1])], ncl, stats
 
 

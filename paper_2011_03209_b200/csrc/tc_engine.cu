@@ -1,17 +1,697 @@
-// tc_engine.cu — tcgen05 candidate engine (placeholder until implemented).
+// tc_engine.cu — eps-adjacency on the 5th-gen tensor cores (tcgen05 + TMEM +
+// TMA), with an exact fp64 recheck of the pairs the tensor cores cannot
+// decide. Reference decision: sqrt(fp64 sum (x_i - x_j)^2 in the element's
+// order) <= eps (clustering.py:113,137-139,166-187).
+//
+// Why integers: the reference's decision is an fp64 comparison, so the
+// candidate distance must come with a RIGOROUS error bound. Floating-point
+// MMA accumulation has no documented rounding model; integer MMA
+// (kind::i8, s32 accumulate) is exact. Each element is centred (c_k) and
+// quantised to 24-bit fixed point q = rint((x - c_k) / s_k), split into
+// three 8-bit limbs q = H*2^16 + M*2^8 + L (H signed, M/L unsigned). The
+// dot product q_i.q_j is the exact sum of 9 limb products; 8 run on the
+// tensor cores (the L.L term, 0 <= LL <= 255^2 d, is bounded instead),
+// accumulated per shift class in 4 TMEM accumulators:
+//   A0 = H.H  A1 = H.M + M.H  A2 = H.L + M.M + L.H  A3 = M.L + L.M
+// D2c = N_i + N_j - 2 (A0<<32 + A1<<24 + A2<<16 + A3<<8) is an exact int64
+// with D2_q in [D2c - 2*LLmax, D2c], where D2_q = |q_i - q_j|^2.
+// Per point the quantisation error e_i = |x_i - c - s q_i| is measured in
+// fp64; by the triangle inequality |d_true - s sqrt(D2_q)| <= e_i + e_j, and
+// the reference's own fp64 result satisfies |d_ref - d_true| <= gamma d_true.
+// Each 128x64 pair tile gets integer thresholds T_in <= T_out:
+//   D2c <= T_in  -> certainly inside (d_ref <= eps)
+//   D2c >  T_out -> certainly outside
+//   otherwise    -> queued and decided by the exact fp64 recheck kernel in
+//                   the element's summation order.
+//
+// Kernel: persistent, one CTA per SM, 256 threads. Warp 0 = TMA producer,
+// warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator, warps 4-7 =
+// epilogue (TMEM lanes = rows). A work unit is (element, 128-row tile I,
+// range of 64-row B tiles); the A tile (3 limb planes x Kpad bytes x 128
+// rows, SW128 K-major) stays resident while B tiles stream through a 2-stage
+// TMA ring; accumulators are double-buffered in TMEM (2 x 4 x 64 columns)
+// so the epilogue of tile b overlaps the MMAs of tile b+1.
+#include <cuda.h>
+
+#include <algorithm>
 #include <vector>
 
 #include "dbscan.cuh"
 
 namespace bm {
 
-bool tc_supported(int64_t d) { (void)d; return false; }
+int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
+                        double eps, uint32_t* adj, cudaStream_t stream);
 
-int tc_build_adjacency(const double*, int64_t, const ElemTables&, int64_t, int64_t, double,
-                       uint32_t*, const uint8_t*, const std::vector<int32_t>&, int64_t*,
-                       cudaStream_t) {
-  set_error("tensor-core engine not built");
-  return BM_ERR_INTERNAL;
+namespace {
+
+constexpr int kBM = 128;        // A rows (TMEM lanes)
+constexpr int kBN = 64;         // B rows per tile (MMA N)
+constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
+constexpr int kStages = 2;      // B ring depth
+constexpr int kUnitB = 16;      // B tiles per work unit (<= 8 bitmap tiles)
+constexpr int kThreads = 256;
+constexpr int kQBits = 23;      // |q| <= 2^23 - 1
+
+struct Unit {
+  int32_t k, I, b0, b1;
+};
+
+__constant__ PwProgram c_prog_tc;
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(b))
+      : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8, s32 accumulate
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::i8: D=s32, A/B K-major, M=128, N=64.
+__host__ __device__ constexpr uint32_t idesc_i8(bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+}
+
+struct TcParams {
+  ElemTables et;
+  const Unit* units;
+  int64_t n_units;
+  const int64_t* nq;      // per padded row: sum q^2
+  const double* tile_e;   // per 128-row tile (global tile index): max quantisation error
+  const int32_t* tbase;   // per element: first global 128-row tile index
+  const double* scale;    // per element s_k
+  double eps;
+  double gamma;           // relative bound |d_ref - d_true| <= gamma d_true
+  int64_t ll2;            // 2 * 255^2 * Kpad
+  int nkc;                // Kpad / 128
+  uint32_t* adj;
+  int2* queue;
+  unsigned long long* qcount;
+  unsigned long long qcap;
+};
+
+__device__ __forceinline__ int64_t clamp_i64(double v) {
+  if (!(v == v)) return 0;
+  if (v >= 4.0e18) return (int64_t)4000000000000000000ll;
+  if (v <= -4.0e18) return -(int64_t)4000000000000000000ll;
+  return (int64_t)v;
+}
+
+// Integer thresholds of one (row tile, column tile) pair; see file header.
+__device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI, int64_t tJ,
+                                           int64_t& t_in, int64_t& t_out) {
+  const double s = P.scale[k];
+  const double delta = P.tile_e[tI] + P.tile_e[tJ];
+  if (!(delta < 1e300) || !(s > 0.0)) {  // NaN/inf inputs: every pair goes to the recheck
+    t_in = -(int64_t)4000000000000000000ll;
+    t_out = (int64_t)4000000000000000000ll;
+    return;
+  }
+  const double a_in = P.eps / (1.0 + P.gamma) - delta;
+  const double a_out = P.eps / (1.0 - P.gamma) + delta;
+  if (a_in > 0.0) {
+    const double r = a_in / s;
+    t_in = clamp_i64(floor(r * r * (1.0 - 1e-12))) - 2;
+  } else {
+    t_in = -(int64_t)4000000000000000000ll;
+  }
+  const double r2 = a_out / s;
+  t_out = clamp_i64(ceil(r2 * r2 * (1.0 + 1e-12))) + P.ll2 + 2;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nkc = P.nkc;
+  const uint32_t a_plane_bytes = (uint32_t)nkc * kBM * kKC;   // per limb plane
+  const uint32_t b_plane_bytes = (uint32_t)nkc * kBN * kKC;
+  const uint32_t a_bytes = 3 * a_plane_bytes;
+  const uint32_t b_bytes = 3 * b_plane_bytes;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + a_bytes;
+  uint64_t* bars = (uint64_t*)(sB + kStages * b_bytes);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 1;
+  uint64_t* b_full = bars + 2;                // [kStages]
+  uint64_t* b_empty = b_full + kStages;       // [kStages]
+  uint64_t* acc_full = b_empty + kStages;     // [2]
+  uint64_t* acc_empty = acc_full + 2;         // [2]
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qmap) : "memory");
+      uint32_t a_empty_ph = 0, stage = 0, ph_empty[kStages] = {0, 0};
+      for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+        const Unit un = P.units[u];
+        const int pb = P.et.pbase[un.k];
+        mbar_wait(a_empty, a_empty_ph ^ 1);
+        a_empty_ph ^= 1;
+        mbar_expect_tx(a_full, a_bytes);
+        for (int pl = 0; pl < 3; ++pl)
+          for (int c = 0; c < nkc; ++c)
+            for (int h = 0; h < 2; ++h)
+              tma_load_3d(sA + pl * a_plane_bytes + (c * kBM + h * 64) * kKC, &qmap, a_full,
+                          c * kKC, pb + un.I * kBM + h * 64, pl);
+        for (int b = un.b0; b < un.b1; ++b) {
+          mbar_wait(b_empty + stage, ph_empty[stage] ^ 1);
+          ph_empty[stage] ^= 1;
+          mbar_expect_tx(b_full + stage, b_bytes);
+          uint8_t* dst = sB + stage * b_bytes;
+          for (int pl = 0; pl < 3; ++pl)
+            for (int c = 0; c < nkc; ++c)
+              tma_load_3d(dst + pl * b_plane_bytes + c * kBN * kKC, &qmap, b_full + stage,
+                          c * kKC, pb + b * kBN, pl);
+          stage = (stage + 1) % kStages;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t ID_SS = idesc_i8(true, true);
+      constexpr uint32_t ID_SU = idesc_i8(true, false);
+      constexpr uint32_t ID_US = idesc_i8(false, true);
+      constexpr uint32_t ID_UU = idesc_i8(false, false);
+      uint32_t a_full_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
+      uint32_t buf = 0, ph_acc_empty[2] = {0, 0};
+      const uint32_t sA_addr = smem_u32(sA);
+      for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+        const Unit un = P.units[u];
+        mbar_wait(a_full, a_full_ph);
+        a_full_ph ^= 1;
+        tc_fence_after();
+        for (int b = un.b0; b < un.b1; ++b) {
+          mbar_wait(b_full + stage, ph_full[stage]);
+          ph_full[stage] ^= 1;
+          mbar_wait(acc_empty + buf, ph_acc_empty[buf] ^ 1);
+          ph_acc_empty[buf] ^= 1;
+          tc_fence_after();
+          const uint32_t sB_addr = smem_u32(sB + stage * b_bytes);
+          const uint32_t acc = tmem_base + buf * 4 * kBN;
+          for (int c = 0; c < nkc; ++c) {
+            for (int kk = 0; kk < kKC / 32; ++kk) {
+              const uint32_t off = c * kBM * kKC + kk * 32;
+              const uint32_t offb = c * kBN * kKC + kk * 32;
+              const uint64_t aH = smem_desc(sA_addr + 0 * a_plane_bytes + off);
+              const uint64_t aM = smem_desc(sA_addr + 1 * a_plane_bytes + off);
+              const uint64_t aL = smem_desc(sA_addr + 2 * a_plane_bytes + off);
+              const uint64_t bH = smem_desc(sB_addr + 0 * b_plane_bytes + offb);
+              const uint64_t bM = smem_desc(sB_addr + 1 * b_plane_bytes + offb);
+              const uint64_t bL = smem_desc(sB_addr + 2 * b_plane_bytes + offb);
+              const uint32_t first = (c == 0 && kk == 0) ? 0u : 1u;
+              mma_i8(acc + 0 * kBN, aH, bH, ID_SS, first);
+              mma_i8(acc + 1 * kBN, aH, bM, ID_SU, first);
+              mma_i8(acc + 1 * kBN, aM, bH, ID_US, 1u);
+              mma_i8(acc + 2 * kBN, aH, bL, ID_SU, first);
+              mma_i8(acc + 2 * kBN, aM, bM, ID_UU, 1u);
+              mma_i8(acc + 2 * kBN, aL, bH, ID_US, 1u);
+              mma_i8(acc + 3 * kBN, aM, bL, ID_UU, first);
+              mma_i8(acc + 3 * kBN, aL, bM, ID_UU, 1u);
+            }
+          }
+          tc_commit(b_empty + stage);   // B slot reusable once these MMAs finish
+          tc_commit(acc_full + buf);    // accumulators ready for the epilogue
+          stage = (stage + 1) % kStages;
+          buf ^= 1;
+        }
+        tc_commit(a_empty);             // A tile reusable
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;           // TMEM lane quarter
+    const int row = ew * 32 + lane;    // A-tile row of this thread
+    uint32_t buf = 0, ph_full[2] = {0, 0};
+    for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+      const Unit un = P.units[u];
+      const int k = un.k;
+      const int pb = P.et.pbase[k];
+      const int n_k = P.et.nrows[k];
+      const int64_t T = P.et.ntiles[k];
+      const int gi = un.I * kBM + row;                // local row index
+      const bool row_ok = gi < n_k;
+      const int64_t nrow = P.nq[pb + gi];
+      const int64_t tI = P.tbase[k] + un.I;
+      for (int b = un.b0; b < un.b1; ++b) {
+        const int J = b >> 1, half = b & 1;
+        int64_t t_in, t_out;
+        thresholds(P, k, tI, P.tbase[k] + J, t_in, t_out);
+        mbar_wait(acc_full + buf, ph_full[buf]);
+        ph_full[buf] ^= 1;
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + buf * 4 * kBN;
+        uint32_t words[2] = {0u, 0u};
+        uint64_t band = 0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kBN; c0 += 16) {
+          int32_t a0[16], a1[16], a2[16], a3[16];
+          tmem_ld16(tacc + 0 * kBN + c0, a0);
+          tmem_ld16(tacc + 1 * kBN + c0, a1);
+          tmem_ld16(tacc + 2 * kBN + c0, a2);
+          tmem_ld16(tacc + 3 * kBN + c0, a3);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int gc = b * kBN + c0 + j;           // local column index
+            const int64_t g = ((int64_t)a0[j] << 32) + ((int64_t)a1[j] << 24) +
+                              ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
+            const int64_t d2 = nrow + __ldg(P.nq + pb + gc) - 2 * g;
+            const bool ok = row_ok && gc < n_k;
+            const bool in = ok && d2 <= t_in;
+            const bool amb = ok && d2 > t_in && d2 <= t_out;
+            const int bit = c0 + j;
+            words[bit >> 5] |= (in ? 1u : 0u) << (bit & 31);
+            band |= (amb ? 1ull : 0ull) << bit;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + buf);
+        buf ^= 1;
+        // bitmap words of (row, 32-col groups 2*half, 2*half+1) in tile (I, J)
+        const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
+        uint2* dst = reinterpret_cast<uint2*>(P.adj + tile * kTileWords + row * 4 + half * 2);
+        *dst = make_uint2(words[0], words[1]);
+        if (band) {
+          const unsigned long long nb = __popcll(band);
+          const unsigned long long at = atomicAdd(P.qcount, nb);
+          unsigned long long i = at;
+          while (band) {
+            const int bit = __ffsll(band) - 1;
+            band &= band - 1;
+            if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + b * kBN + bit);
+            ++i;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// preparation: per-element centre / scale, quantisation, per-tile error max
+// ---------------------------------------------------------------------------
+// per 128-row tile (global tile index t): column min/max over valid rows
+__global__ void tile_minmax_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+                                   const int32_t* __restrict__ tile_elem, int64_t n_tiles,
+                                   double* __restrict__ tmin, double* __restrict__ tmax) {
+  const int64_t t = blockIdx.x;
+  if (t >= n_tiles) return;
+  const int k = tile_elem[t];
+  const int64_t p0 = t * kTile;  // padded base of this tile
+  const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    for (int r = 0; r < valid; ++r) {
+      const double v = Xg[(p0 + r) * d + c];
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+    }
+    tmin[t * d + c] = mn;
+    tmax[t * d + c] = mx;
+  }
+}
+
+// per element: centre c = (min+max)/2 per column, half-range R, scale s
+__global__ void elem_scale_kernel(int64_t d, ElemTables et, const int32_t* __restrict__ tbase,
+                                  const double* __restrict__ tmin,
+                                  const double* __restrict__ tmax, double* __restrict__ center,
+                                  double* __restrict__ scale) {
+  const int k = blockIdx.x;
+  const int64_t t0 = tbase[k], t1 = tbase[k] + et.ntiles[k];
+  __shared__ double red[256];
+  double R = 0.0;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    for (int64_t t = t0; t < t1; ++t) {
+      mn = fmin(mn, tmin[t * d + c]);
+      mx = fmax(mx, tmax[t * d + c]);
+    }
+    double cc = t1 > t0 ? 0.5 * mn + 0.5 * mx : 0.0;
+    if (!(cc == cc) || t1 == t0) cc = 0.0;
+    center[(int64_t)k * d + c] = cc;
+    if (t1 > t0) R = fmax(R, fmax(mx - cc, cc - mn));
+  }
+  red[threadIdx.x] = R;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double Rk = red[0] * (1.0 + 1e-12);
+    scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
+  }
+}
+
+// one warp per padded row: limbs into the three planes, N = sum q^2 (exact),
+// e = |x - c - s q| (fp64) -> tile max via atomicMax on the bit pattern
+__global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad,
+                                ElemTables et, int64_t P, const double* __restrict__ center,
+                                const double* __restrict__ scale, int8_t* __restrict__ planes,
+                                int64_t* __restrict__ nq, unsigned long long* __restrict__ tile_e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
+       p += (int64_t)gridDim.x * wpb) {
+    int64_t a = 0, bb = et.n_el;
+    while (bb - a > 1) {
+      int64_t mid = (a + bb) >> 1;
+      if (et.pbase[mid] <= p) a = mid; else bb = mid;
+    }
+    const int k = (int)a;
+    const bool valid = (p - et.pbase[k]) < et.nrows[k];
+    const double s = scale[k];
+    const double inv = 1.0 / s;
+    long long nsum = 0;
+    double esum = 0.0, ysum = 0.0;
+    int8_t* hp = planes + p * kpad;
+    uint8_t* mp = (uint8_t*)planes + P * kpad + p * kpad;
+    uint8_t* lp = (uint8_t*)planes + 2 * P * kpad + p * kpad;
+    for (int64_t c = lane; c < kpad; c += 32) {
+      int q = 0;
+      if (valid && c < d) {
+        const double y = Xg[p * d + c] - center[(int64_t)k * d + c];
+        double qd = rint(y * inv);
+        qd = fmin(fmax(qd, -(double)((1 << kQBits) - 1)), (double)((1 << kQBits) - 1));
+        q = (int)qd;
+        const double e = y - qd * s;
+        esum += e * e;
+        ysum += y * y;
+      }
+      nsum += (long long)q * q;
+      hp[c] = (int8_t)(q >> 16);
+      mp[c] = (uint8_t)((q >> 8) & 255);
+      lp[c] = (uint8_t)(q & 255);
+    }
+    for (int o = 16; o; o >>= 1) {
+      nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      esum += __shfl_xor_sync(0xffffffffu, esum, o);
+      ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
+    }
+    if (lane == 0) {
+      nq[p] = nsum;
+      if (valid) {
+        // rigorous upper bound of |x - c - s q|: the fp64 evaluation of each
+        // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
+        const double e = sqrt(esum) * (1.0 + 1e-12) + 1e-15 * sqrt(ysum) + 1e-300;
+        atomicMax(tile_e + p / kTile, (unsigned long long)__double_as_longlong(e));
+      }
+    }
+  }
+}
+
+// exact recheck of the queued pairs in the element's fp64 order
+__global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+                               const int2* __restrict__ queue, int64_t nq, double eps,
+                               uint32_t* __restrict__ adj,
+                               unsigned long long* __restrict__ n_inside) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int2 pr = queue[i];
+    int64_t a = 0, bb = et.n_el;
+    while (bb - a > 1) {
+      int64_t mid = (a + bb) >> 1;
+      if (et.pbase[mid] <= pr.x) a = mid; else bb = mid;
+    }
+    const int k = (int)a;
+    const double s2 = exact_dist2(Xg + (int64_t)pr.x * d, Xg + (int64_t)pr.y * d, d,
+                                  et.order[k], c_prog_tc);
+    if (__dsqrt_rn(s2) <= eps) {
+      const int li = pr.x - et.pbase[k], lj = pr.y - et.pbase[k];
+      const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
+      const int64_t tile = et.tp_off[k] + tri_index(I, J, et.ntiles[k]);
+      atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
+      atomicAdd(n_inside, 1ull);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptor through the driver entry point (no libcuda link dependency)
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_qmap(CUtensorMap* map, void* planes, int64_t P, int64_t kpad) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    BM_CHECK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return BM_ERR_INTERNAL;
+    }
+    fn = (EncodeTiledFn)p;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)kpad, (cuuint64_t)P, 3};
+  cuuint64_t strides[2] = {(cuuint64_t)kpad, (cuuint64_t)(P * kpad)};
+  cuuint32_t box[3] = {(cuuint32_t)kKC, (cuuint32_t)64, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return BM_ERR_INTERNAL;
+  }
+  return BM_OK;
+}
+
+inline unsigned grid_cap(int64_t n, int threads, int per_sm) {
+  int64_t b = ceil_div(n, threads);
+  int64_t cap = (int64_t)num_sms() * per_sm;
+  return (unsigned)std::max<int64_t>(1, std::min(b, cap));
+}
+
+}  // namespace
+
+bool tc_supported(int64_t d) { return d >= 32 && d <= 256; }
+
+int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, int64_t P,
+                       double eps, uint32_t* adj, const uint8_t* h_order,
+                       const std::vector<int32_t>& h_nrows, int64_t* stats,
+                       cudaStream_t stream) {
+  (void)h_order;
+  const int64_t n_el = et.n_el;
+  const int64_t kpad = ceil_div(d, kKC) * kKC;
+  const int nkc = (int)(kpad / kKC);
+  BM_REQUIRE(nkc >= 1 && nkc <= 2, "tensor-core engine supports d <= 256");
+  PwProgram prog;
+  BM_TRY(make_pw_program(d, &prog));
+  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog_tc, &prog, sizeof(prog), 0,
+                                        cudaMemcpyHostToDevice, stream));
+
+  // ---- host tables: tile -> element, element tile base, work units
+  const int64_t n_tiles = P / kTile;
+  std::vector<int32_t> tile_elem(n_tiles), tbase(n_el + 1, 0);
+  std::vector<Unit> units;
+  for (int64_t k = 0; k < n_el; ++k) {
+    const int64_t T = ceil_div(h_nrows[k], kTile);
+    tbase[k + 1] = (int32_t)(tbase[k] + T);
+    for (int64_t t = 0; t < T; ++t) tile_elem[tbase[k] + t] = (int32_t)k;
+    for (int64_t I = 0; I < T; ++I)
+      for (int64_t b0 = 2 * I; b0 < 2 * T; b0 += kUnitB)
+        units.push_back({(int32_t)k, (int32_t)I, (int32_t)b0,
+                         (int32_t)std::min<int64_t>(b0 + kUnitB, 2 * T)});
+  }
+  const int64_t n_units = (int64_t)units.size();
+  if (n_units == 0) return BM_OK;
+
+  // ---- device buffers
+  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_units, s_q, s_cnt;
+  BM_TRY(scratch_alloc(s_tab, (n_tiles + n_el + 1) * 4 + 16, stream));
+  int32_t* d_tile_elem = s_tab.as<int32_t>();
+  int32_t* d_tbase = d_tile_elem + n_tiles;
+  BM_CHECK_CUDA(cudaMemcpyAsync(d_tile_elem, tile_elem.data(), n_tiles * 4,
+                                cudaMemcpyHostToDevice, stream));
+  BM_CHECK_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), (n_el + 1) * 4, cudaMemcpyHostToDevice,
+                                stream));
+  BM_TRY(scratch_alloc(s_mm, (size_t)n_tiles * d * 16, stream));
+  double* tmin = s_mm.as<double>();
+  double* tmax = tmin + n_tiles * d;
+  BM_TRY(scratch_alloc(s_cs, (size_t)(n_el * d + n_el) * 8, stream));
+  double* center = s_cs.as<double>();
+  double* scale = center + n_el * d;
+  BM_TRY(scratch_alloc(s_pl, (size_t)3 * P * kpad, stream));
+  BM_TRY(scratch_alloc(s_nq, (size_t)P * 8, stream));
+  BM_TRY(scratch_alloc(s_te, (size_t)n_tiles * 8, stream));
+  BM_CHECK_CUDA(cudaMemsetAsync(s_te.ptr, 0, n_tiles * 8, stream));
+  BM_TRY(scratch_alloc(s_units, n_units * sizeof(Unit), stream));
+  BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, units.data(), n_units * sizeof(Unit),
+                                cudaMemcpyHostToDevice, stream));
+
+  tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, d_tile_elem, n_tiles, tmin,
+                                                            tmax);
+  BM_CHECK_LAUNCH();
+  elem_scale_kernel<<<(unsigned)n_el, 256, 0, stream>>>(d, et, d_tbase, tmin, tmax, center,
+                                                        scale);
+  BM_CHECK_LAUNCH();
+  quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
+      Xg, d, kpad, et, P, center, scale, s_pl.as<int8_t>(), s_nq.as<int64_t>(),
+      s_te.as<unsigned long long>());
+  BM_CHECK_LAUNCH();
+
+  CUtensorMap qmap;
+  BM_TRY(make_qmap(&qmap, s_pl.ptr, P, kpad));
+
+  // ---- MMA pass (re-run with a larger recheck queue on overflow)
+  int64_t pairs = 0;
+  for (int64_t k = 0; k < n_el; ++k) pairs += (int64_t)h_nrows[k] * h_nrows[k];
+  unsigned long long qcap = std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 5000));
+  BM_TRY(scratch_alloc(s_cnt, 16, stream));
+  unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
+  const size_t smem = 1024 + 3 * (size_t)nkc * kKC * (kBM + kStages * kBN) + 256;
+  static bool attr = false;
+  if (!attr) {
+    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
+  unsigned long long h_cnt[2] = {0, 0};
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    BM_TRY(scratch_alloc(s_q, qcap * sizeof(int2), stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
+    TcParams prm{et,   s_units.as<Unit>(), n_units, s_nq.as<int64_t>(), nullptr, d_tbase,
+                 scale, eps, gamma, (int64_t)2 * 255 * 255 * kpad, nkc, adj, s_q.as<int2>(),
+                 d_cnt, qcap};
+    prm.tile_e = reinterpret_cast<const double*>(s_te.ptr);
+    const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
+    tc_adjacency_kernel<<<grid, kThreads, smem, stream>>>(qmap, prm);
+    BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    if (h_cnt[0] <= qcap) break;
+    qcap = h_cnt[0] + 1024;
+    if (attempt == 2) {
+      set_error("recheck queue overflow");
+      return BM_ERR_INTERNAL;
+    }
+  }
+  const int64_t nrec = (int64_t)h_cnt[0];
+  if (nrec > 0) {
+    recheck_kernel<<<grid_cap(nrec, 128, 16), 128, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
+                                                                eps, adj, d_cnt + 1);
+    BM_CHECK_LAUNCH();
+  }
+  stats[0] += pairs;
+  stats[1] += nrec;
+  return BM_OK;
 }
 
 }  // namespace bm

@@ -55,6 +55,9 @@ int bm_abi_version(void);
 const char* bm_last_error(void);
 /* Kernel launches issued by this library since load (benchmark evidence). */
 int64_t bm_launch_count(void);
+/* Internal scratch is stream-ordered pool memory kept mapped between calls
+ * (re-mapping GBs per call is slow); this returns it to the driver. */
+int bm_release_scratch(void);
 /* Number of visible CUDA devices (for the host-side GPU-count knob). */
 int bm_device_count(int* out);
 
@@ -101,7 +104,7 @@ int bm_membership_fill(const double* d_f, int64_t n, int m, const double* h_lo,
  * engine: BM_ENGINE_*.  stats (optional, 8 int64): [0] pairs evaluated,
  * [1] pairs rechecked in exact fp64, [2] tiles skipped, [3] tile pairs total,
  * [4] adjacency bytes, [5] adjacency-stage device time (ns, CUDA events on
- * `stream`), [6..7] reserved. */
+ * `stream`), [6] gather/setup time (ns), [7] counts/union-find/relabel time (ns). */
 int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
                         const int64_t* d_rows, const int64_t* h_offsets,
                         int64_t n_el, double eps, int32_t min_pts,

@@ -1,5 +1,6 @@
 // common.cu — error state, scratch allocation and device-wide scans.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include <atomic>
 #include <mutex>
@@ -24,7 +25,38 @@ void set_error(const char* fmt, ...) {
 
 const char* get_error() { return g_err.c_str(); }
 
+// Scratch comes from the device's default stream-ordered pool. Its release
+// threshold is raised once per device so freed blocks stay mapped between
+// calls: re-mapping the ~12 GB a 1M-point build uses costs ~0.5 s per call.
+// B200MAP_POOL_RELEASE=1 restores the CUDA default (return memory at sync).
+static void retain_pool_once() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 64 || done[dev]) return;
+  done[dev] = true;
+  const char* env = getenv("B200MAP_POOL_RELEASE");
+  if (env && env[0] == '1') return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+}
+
+void release_pool() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+}
+
 int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
+  retain_pool_once();
   if (s.ptr) cudaFreeAsync(s.ptr, s.stream);
   s.ptr = nullptr;
   s.bytes = bytes;
@@ -197,6 +229,11 @@ extern "C" {
 int bm_abi_version(void) { return 1; }
 
 int64_t bm_launch_count(void) { return bm::g_launches.load(); }
+
+int bm_release_scratch(void) {
+  bm::release_pool();
+  return BM_OK;
+}
 
 const char* bm_last_error(void) { return bm::get_error(); }
 

@@ -25,7 +25,7 @@
 namespace bm {
 
 int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
-                       int64_t P, double eps, uint32_t* adj, const uint8_t* h_order,
+                       int64_t P, double eps, uint32_t* adj, int32_t* cnt, const uint8_t* h_order,
                        const std::vector<int32_t>& h_nrows, int64_t* stats,
                        cudaStream_t stream);
 bool tc_supported(int64_t d);
@@ -637,32 +637,18 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     ElemTables et{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, nb_el};
 
     // ---- gather rows (fp64, membership order, padded)
+    cudaEvent_t evs = nullptr, ev2 = nullptr;
+    BM_CHECK_CUDA(cudaEventCreate(&evs));
+    BM_CHECK_CUDA(cudaEventCreate(&ev2));
+    BM_CHECK_CUDA(cudaEventRecord(evs, stream));
     Scratch xg;
     BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
     gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(
         d_X, d, d_rows + h_offsets[bt.k0], d_offs, et, P, xg.as<double>());
     BM_CHECK_LAUNCH();
 
-    // ---- adjacency bitmap
-    Scratch adj;
-    BM_TRY(scratch_alloc(adj, (size_t)n_tp * kTileWords * 4, stream));
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    BM_CHECK_CUDA(cudaEventCreate(&ev0));
-    BM_CHECK_CUDA(cudaEventCreate(&ev1));
-    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
-    if (use_tc) {
-      BM_TRY(tc_build_adjacency(xg.as<double>(), d, et, n_tp, P, eps, adj.as<uint32_t>(),
-                                order.data(), nrows, stats, stream));
-    } else {
-      BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, n_tp, eps, adj.as<uint32_t>(),
-                                   stream));
-      for (int64_t i = 0; i < nb_el; ++i) stats[0] += (int64_t)nrows[i] * (nrows[i] + 1) / 2;
-    }
-    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
-    stats[3] += n_tp;
-    stats[4] = std::max<int64_t>(stats[4], n_tp * kTileWords * 4);
-
-    // ---- counts, core, union-find, border
+    // ---- per-row work arrays (counts are filled by the adjacency stage for
+    //      the tensor-core engine, by count_kernel for the exact engine)
     Scratch work;
     size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
     BM_TRY(scratch_alloc(work, wbytes, stream));
@@ -677,8 +663,31 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
     const unsigned tgrid = grid_for(n_tp, 1, 32);
-    count_kernel<<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, cnt);
-    BM_CHECK_LAUNCH();
+
+    // ---- adjacency bitmap
+    Scratch adj;
+    BM_TRY(scratch_alloc(adj, (size_t)n_tp * kTileWords * 4, stream));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    BM_CHECK_CUDA(cudaEventCreate(&ev0));
+    BM_CHECK_CUDA(cudaEventCreate(&ev1));
+    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+    if (use_tc) {
+      BM_TRY(tc_build_adjacency(xg.as<double>(), d, et, n_tp, P, eps, adj.as<uint32_t>(), cnt,
+                                order.data(), nrows, stats, stream));
+    } else {
+      BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, n_tp, eps, adj.as<uint32_t>(),
+                                   stream));
+      for (int64_t i = 0; i < nb_el; ++i) stats[0] += (int64_t)nrows[i] * (nrows[i] + 1) / 2;
+    }
+    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+    stats[3] += n_tp;
+    stats[4] = std::max<int64_t>(stats[4], n_tp * kTileWords * 4);
+
+    // ---- counts, core, union-find, border
+    if (!use_tc) {
+      count_kernel<<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, cnt);
+      BM_CHECK_LAUNCH();
+    }
     core_init_kernel<<<grid_for(P, 256), 256, 0, stream>>>(cnt, et, P, min_pts, core, par, bmin);
     BM_CHECK_LAUNCH();
     components_kernel<true><<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, core, par,
@@ -704,14 +713,21 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(
         et, d_offs, n_entries, lab, cmin, hscan, d_labels + h_offsets[bt.k0]);
     BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(h_n_clusters + bt.k0, ncl_d.ptr, nb_el * 4,
                                   cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
-    float ms = 0.f;
+    float ms = 0.f, ms_pre = 0.f, ms_post = 0.f;
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    stats[5] += (int64_t)(ms * 1e6);  // adjacency (distance) stage, ns on the launch stream
+    BM_CHECK_CUDA(cudaEventElapsedTime(&ms_pre, evs, ev0));
+    BM_CHECK_CUDA(cudaEventElapsedTime(&ms_post, ev1, ev2));
+    stats[5] += (int64_t)(ms * 1e6);       // adjacency (distance) stage, ns on the launch stream
+    stats[6] += (int64_t)(ms_pre * 1e6);   // gather + setup
+    stats[7] += (int64_t)(ms_post * 1e6);  // counts, union-find, border, relabel
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
+    cudaEventDestroy(evs);
+    cudaEventDestroy(ev2);
   }
   return BM_OK;
 }

@@ -49,8 +49,9 @@ constexpr int kBM = 128;        // A rows (TMEM lanes)
 constexpr int kBN = 64;         // B rows per tile (MMA N)
 constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
 constexpr int kStages = 2;      // B ring depth
-constexpr int kUnitB = 16;      // B tiles per work unit (<= 8 bitmap tiles)
-constexpr int kThreads = 256;
+constexpr int kUnitB = 32;      // B tiles per work unit (<= 16 bitmap tiles)
+constexpr int kEpiWarps = 8;    // epilogue warps 4..11
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kQBits = 23;      // |q| <= 2^23 - 1
 
 struct Unit {
@@ -119,15 +120,6 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -155,46 +147,53 @@ struct TcParams {
   const Unit* units;
   int64_t n_units;
   const int64_t* nq;      // per padded row: sum q^2
-  const double* tile_e;   // per 128-row tile (global tile index): max quantisation error
+  const double* tile_u;   // per 128-row tile: max quantisation error / s_k (quantised units)
   const int32_t* tbase;   // per element: first global 128-row tile index
-  const double* scale;    // per element s_k
-  double eps;
-  double gamma;           // relative bound |d_ref - d_true| <= gamma d_true
-  int64_t ll2;            // 2 * 255^2 * Kpad
+  const double* a_in;     // per element: eps / (1 + gamma) / s_k
+  const double* a_out;    // per element: eps / (1 - gamma) / s_k
+  double ll2;             // 2 * 255^2 * Kpad (bound of the omitted L.L term in D2)
+  double a3max;           // 2^9 * 2 * 255^2 * Kpad (bound of the A3 term in D2)
   int nkc;                // Kpad / 128
   uint32_t* adj;
+  int32_t* cnt;           // eps-neighbour counts per padded row (self included)
   int2* queue;
   unsigned long long* qcount;
   unsigned long long qcap;
 };
 
-__device__ __forceinline__ int64_t clamp_i64(double v) {
-  if (!(v == v)) return 0;
-  if (v >= 4.0e18) return (int64_t)4000000000000000000ll;
-  if (v <= -4.0e18) return -(int64_t)4000000000000000000ll;
-  return (int64_t)v;
-}
+constexpr double kBig = 4.0e18;
 
-// Integer thresholds of one (row tile, column tile) pair; see file header.
+// fp64 thresholds on D2c for one (row tile, column tile) pair; the +-64
+// margins cover the fp64 rounding of S = N_i + N_j and of the fast D2.
 __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI, int64_t tJ,
-                                           int64_t& t_in, int64_t& t_out) {
-  const double s = P.scale[k];
-  const double delta = P.tile_e[tI] + P.tile_e[tJ];
-  if (!(delta < 1e300) || !(s > 0.0)) {  // NaN/inf inputs: every pair goes to the recheck
-    t_in = -(int64_t)4000000000000000000ll;
-    t_out = (int64_t)4000000000000000000ll;
+                                           double& t_in, double& t_out) {
+  const double du = P.tile_u[tI] + P.tile_u[tJ];
+  if (!(du < 1e300)) {  // NaN/inf inputs: every pair of the tile goes to the recheck
+    t_in = -kBig;
+    t_out = kBig;
     return;
   }
-  const double a_in = P.eps / (1.0 + P.gamma) - delta;
-  const double a_out = P.eps / (1.0 - P.gamma) + delta;
-  if (a_in > 0.0) {
-    const double r = a_in / s;
-    t_in = clamp_i64(floor(r * r * (1.0 - 1e-12))) - 2;
-  } else {
-    t_in = -(int64_t)4000000000000000000ll;
-  }
-  const double r2 = a_out / s;
-  t_out = clamp_i64(ceil(r2 * r2 * (1.0 + 1e-12))) + P.ll2 + 2;
+  const double ri = P.a_in[k] - du;
+  t_in = ri > 0.0 ? ri * ri * (1.0 - 1e-12) - 64.0 : -kBig;
+  const double ro = P.a_out[k] + du;
+  t_out = ro * ro * (1.0 + 1e-12) + P.ll2 + 64.0;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -216,6 +215,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   uint64_t* acc_full = b_empty + kStages;     // [2]
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+  int32_t* colcnt = (int32_t*)(tmem_slot + 4);            // [2][kBN]
+  double* ncol = (double*)(colcnt + 2 * kBN);             // [kEpiWarps][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -227,10 +228,11 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, 4);
+      mbar_init(acc_empty + s, kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < 2 * kBN; i += blockDim.x) colcnt[i] = 0;
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tmem_slot)));
@@ -324,8 +326,12 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 4;           // TMEM lane quarter
-    const int row = ew * 32 + lane;    // A-tile row of this thread
+    // warp (q, ch): TMEM lane quarter q (rows 32q..32q+31), column half ch
+    const int ew = warp - 4;
+    const int q = warp & 3;            // tcgen05.ld lane window = warp % 4
+    const int ch = ew >> 2;
+    const int row = q * 32 + lane;
+    double* my_ncol = ncol + ew * 32;
     uint32_t buf = 0, ph_full[2] = {0, 0};
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
       const Unit un = P.units[u];
@@ -335,60 +341,96 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const int64_t T = P.et.ntiles[k];
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
-      const int64_t nrow = P.nq[pb + gi];
+      const double nrow = (double)P.nq[pb + gi];
       const int64_t tI = P.tbase[k] + un.I;
+      int row_count = 0;
       for (int b = un.b0; b < un.b1; ++b) {
         const int J = b >> 1, half = b & 1;
-        int64_t t_in, t_out;
+        const int col0 = b * kBN + ch * 32;           // first local column of this warp
+        double t_in, t_out;
         thresholds(P, k, tI, P.tbase[k] + J, t_in, t_out);
+        const double t_out_fast = t_out + P.a3max;
+        my_ncol[lane] = (double)P.nq[pb + col0 + lane];
+        const bool col_ok_lane = col0 + lane < n_k;
+        const uint32_t colmask = __ballot_sync(0xffffffffu, col_ok_lane);
         mbar_wait(acc_full + buf, ph_full[buf]);
         ph_full[buf] ^= 1;
         tc_fence_after();
-        const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + buf * 4 * kBN;
-        uint32_t words[2] = {0u, 0u};
-        uint64_t band = 0;
-#pragma unroll 1
-        for (int c0 = 0; c0 < kBN; c0 += 16) {
-          int32_t a0[16], a1[16], a2[16], a3[16];
-          tmem_ld16(tacc + 0 * kBN + c0, a0);
-          tmem_ld16(tacc + 1 * kBN + c0, a1);
-          tmem_ld16(tacc + 2 * kBN + c0, a2);
-          tmem_ld16(tacc + 3 * kBN + c0, a3);
+        const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 4 * kBN + ch * 32;
+        int32_t a0[32], a1[32], a2[32];
+        tmem_ld32(tacc + 0 * kBN, a0);
+        tmem_ld32(tacc + 1 * kBN, a1);
+        tmem_ld32(tacc + 2 * kBN, a2);
+        tmem_ld_wait();
+        __syncwarp();
+        uint32_t in_w = 0, amb_w = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          // exact in fp64: g = 2^8 (2^8 a0 + a1) + a2  (< 2^40)
+          const int t1 = a0[j] * 256 + a1[j];
+          const double g = fma((double)t1, 256.0, (double)a2[j]);
+          const double d2 = fma(-131072.0, g, nrow + my_ncol[j]);  // D2c + 2^9 a3
+          in_w |= (d2 <= t_in ? 1u : 0u) << j;
+          amb_w |= (d2 <= t_out_fast ? 1u : 0u) << j;
+        }
+        const uint32_t valid = row_ok ? colmask : 0u;
+        in_w &= valid;
+        amb_w &= valid & ~in_w;
+        uint32_t band = 0;
+        if (__any_sync(0xffffffffu, amb_w != 0)) {
+          // rare: the omitted A3 term matters -> exact int64 D2c
+          int32_t a3[32];
+          tmem_ld32(tacc + 3 * kBN, a3);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int gc = b * kBN + c0 + j;           // local column index
-            const int64_t g = ((int64_t)a0[j] << 32) + ((int64_t)a1[j] << 24) +
-                              ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
-            const int64_t d2 = nrow + __ldg(P.nq + pb + gc) - 2 * g;
-            const bool ok = row_ok && gc < n_k;
-            const bool in = ok && d2 <= t_in;
-            const bool amb = ok && d2 > t_in && d2 <= t_out;
-            const int bit = c0 + j;
-            words[bit >> 5] |= (in ? 1u : 0u) << (bit & 31);
-            band |= (amb ? 1ull : 0ull) << bit;
+          for (int j = 0; j < 32; ++j) {
+            if (!((amb_w >> j) & 1u)) continue;  // static j keeps a0..a3 in registers
+            const int64_t gg = ((int64_t)a0[j] << 32) + ((int64_t)a1[j] << 24) +
+                               ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
+            const int64_t d2 = P.nq[pb + gi] + P.nq[pb + col0 + j] - 2 * gg;
+            const double dd = (double)d2;  // exact to 1 ulp; margins cover it
+            if (dd <= t_in) in_w |= 1u << j;
+            else if (dd <= t_out) band |= 1u << j;
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + buf);
-        buf ^= 1;
-        // bitmap words of (row, 32-col groups 2*half, 2*half+1) in tile (I, J)
+        // bitmap word (row, 32 columns) of tile (I, J)
         const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
-        uint2* dst = reinterpret_cast<uint2*>(P.adj + tile * kTileWords + row * 4 + half * 2);
-        *dst = make_uint2(words[0], words[1]);
+        P.adj[tile * kTileWords + row * 4 + half * 2 + ch] = in_w;
+        row_count += __popc(in_w);
+        // column counts (off-diagonal tiles only): ballot per column, reduce
+        // the 4 row quarters in smem, one global atomic per column
+        if (J != un.I) {
+          int my = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int c = __popc(__ballot_sync(0xffffffffu, (in_w >> j) & 1u));
+            if (lane == j) my = c;
+          }
+          if (my) atomicAdd(colcnt + buf * kBN + ch * 32 + lane, my);
+        }
+        epi_bar();
+        if (J != un.I && q == 0) {
+          int32_t* cc = colcnt + buf * kBN + ch * 32 + lane;
+          const int v = *cc;
+          if (v) atomicAdd(P.cnt + pb + col0 + lane, v);
+          *cc = 0;
+        }
+        buf ^= 1;
         if (band) {
-          const unsigned long long nb = __popcll(band);
-          const unsigned long long at = atomicAdd(P.qcount, nb);
-          unsigned long long i = at;
+          const unsigned long long nb = __popc(band);
+          unsigned long long i = atomicAdd(P.qcount, nb);
           while (band) {
-            const int bit = __ffsll(band) - 1;
+            const int j = __ffs(band) - 1;
             band &= band - 1;
-            if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + b * kBN + bit);
+            if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + j);
             ++i;
           }
         }
       }
+      if (row_count) atomicAdd(P.cnt + pb + gi, row_count);
     }
   }
   tc_fence_before();
@@ -512,10 +554,30 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
   }
 }
 
+// per tile: quantisation-error bound in quantised units; per element: the
+// eps radii a_in = eps/(1+gamma)/s, a_out = eps/(1-gamma)/s
+__global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ tile_e_bits,
+                                       const int32_t* __restrict__ tile_elem, int64_t n_tiles,
+                                       const double* __restrict__ scale, int64_t n_el, double eps,
+                                       double gamma, double* __restrict__ tile_u,
+                                       double* __restrict__ a_in, double* __restrict__ a_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_tiles) {
+    const double e = __longlong_as_double((long long)tile_e_bits[i]);
+    // round the quotient up: u >= e / s
+    tile_u[i] = __ddiv_ru(e, scale[tile_elem[i]]);
+  }
+  if (i < n_el) {
+    const double s = scale[i];
+    a_in[i] = __ddiv_rd(__ddiv_rd(eps, 1.0 + gamma), s);
+    a_out[i] = __ddiv_ru(__ddiv_ru(eps, 1.0 - gamma), s);
+  }
+}
+
 // exact recheck of the queued pairs in the element's fp64 order
 __global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
                                const int2* __restrict__ queue, int64_t nq, double eps,
-                               uint32_t* __restrict__ adj,
+                               uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
                                unsigned long long* __restrict__ n_inside) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -533,6 +595,8 @@ __global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTab
       const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
       const int64_t tile = et.tp_off[k] + tri_index(I, J, et.ntiles[k]);
       atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
+      atomicAdd(cnt + pr.x, 1);
+      if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
       atomicAdd(n_inside, 1ull);
     }
   }
@@ -583,7 +647,7 @@ inline unsigned grid_cap(int64_t n, int threads, int per_sm) {
 bool tc_supported(int64_t d) { return d >= 32 && d <= 256; }
 
 int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, int64_t P,
-                       double eps, uint32_t* adj, const uint8_t* h_order,
+                       double eps, uint32_t* adj, int32_t* cnt, const uint8_t* h_order,
                        const std::vector<int32_t>& h_nrows, int64_t* stats,
                        cudaStream_t stream) {
   (void)h_order;
@@ -655,7 +719,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   unsigned long long qcap = std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 5000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
-  const size_t smem = 1024 + 3 * (size_t)nkc * kKC * (kBM + kStages * kBN) + 256;
+  const size_t smem = 1024 + 3 * (size_t)nkc * kKC * (kBM + kStages * kBN) + 256 + 4096;
   static bool attr = false;
   if (!attr) {
     BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel,
@@ -663,14 +727,37 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     attr = true;
   }
   const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
+  Scratch s_thr;
+  BM_TRY(scratch_alloc(s_thr, (size_t)(n_tiles + 2 * n_el) * 8, stream));
+  double* tile_u = s_thr.as<double>();
+  double* a_in = tile_u + n_tiles;
+  double* a_out = a_in + n_el;
+  thresholds_prep_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n_tiles, n_el), 256), 256, 0,
+                           stream>>>(s_te.as<unsigned long long>(), d_tile_elem, n_tiles, scale,
+                                     n_el, eps, gamma, tile_u, a_in, a_out);
+  BM_CHECK_LAUNCH();
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
     BM_TRY(scratch_alloc(s_q, qcap * sizeof(int2), stream));
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
-    TcParams prm{et,   s_units.as<Unit>(), n_units, s_nq.as<int64_t>(), nullptr, d_tbase,
-                 scale, eps, gamma, (int64_t)2 * 255 * 255 * kpad, nkc, adj, s_q.as<int2>(),
-                 d_cnt, qcap};
-    prm.tile_e = reinterpret_cast<const double*>(s_te.ptr);
+    BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, (size_t)P * 4, stream));
+    TcParams prm{};
+    prm.et = et;
+    prm.units = s_units.as<Unit>();
+    prm.n_units = n_units;
+    prm.nq = s_nq.as<int64_t>();
+    prm.tile_u = tile_u;
+    prm.tbase = d_tbase;
+    prm.a_in = a_in;
+    prm.a_out = a_out;
+    prm.ll2 = 2.0 * 255.0 * 255.0 * (double)kpad;
+    prm.a3max = 512.0 * 2.0 * 255.0 * 255.0 * (double)kpad;
+    prm.nkc = nkc;
+    prm.adj = adj;
+    prm.cnt = cnt;
+    prm.queue = s_q.as<int2>();
+    prm.qcount = d_cnt;
+    prm.qcap = qcap;
     const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
     tc_adjacency_kernel<<<grid, kThreads, smem, stream>>>(qmap, prm);
     BM_CHECK_LAUNCH();
@@ -686,7 +773,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
     recheck_kernel<<<grid_cap(nrec, 128, 16), 128, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
-                                                                eps, adj, d_cnt + 1);
+                                                                eps, adj, cnt, d_cnt + 1);
     BM_CHECK_LAUNCH();
   }
   stats[0] += pairs;

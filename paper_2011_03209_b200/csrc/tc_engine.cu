@@ -192,6 +192,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
       : "r"(taddr));
 }
 
+// one step of the in-warp 32x32 bit-matrix transpose (lane i holds row i)
+__device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32_t m, int lane) {
+  const uint32_t t = __shfl_xor_sync(0xffffffffu, w, s);
+  return (lane & s) ? ((w & ~m) | ((t >> s) & m)) : ((w & m) | ((t << s) & ~m));
+}
+
 __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
 }
@@ -331,7 +337,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     const int q = warp & 3;            // tcgen05.ld lane window = warp % 4
     const int ch = ew >> 2;
     const int row = q * 32 + lane;
-    double* my_ncol = ncol + ew * 32;
+    int32_t* my_c = reinterpret_cast<int32_t*>(ncol) + ew * 32;  // floor(N_j / 2^25)
     uint32_t buf = 0, ph_full[2] = {0, 0};
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
       const Unit un = P.units[u];
@@ -341,7 +347,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const int64_t T = P.et.ntiles[k];
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
-      const double nrow = (double)P.nq[pb + gi];
+      const int64_t nrow_i = P.nq[pb + gi];
+      const double nrow = (double)nrow_i;
       const int64_t tI = P.tbase[k] + un.I;
       int row_count = 0;
       for (int b = un.b0; b < un.b1; ++b) {
@@ -349,8 +356,20 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         const int col0 = b * kBN + ch * 32;           // first local column of this warp
         double t_in, t_out;
         thresholds(P, k, tI, P.tbase[k] + J, t_in, t_out);
-        const double t_out_fast = t_out + P.a3max;
-        my_ncol[lane] = (double)P.nq[pb + col0 + lane];
+        // Integer fast path. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
+        //   y >= r_in  => D2c <= t_in (certainly inside)
+        //   y <= r_out => D2c >  t_out (certainly outside, A3 and L.L bounded)
+        // (derivation in DESIGN.md; +-1 margins absorb every rounding).
+        int r_in = 0x7fffffff, r_out = (int)0x80000000;
+        if (t_in > -1e18) {
+          const double v = ceil((nrow - t_in) * (1.0 / 33554432.0)) + 2.0;
+          r_in = (int)fmin(fmax(v, -2147483000.0), 2147483000.0);
+        }
+        if (t_out < 1e18) {
+          const double v = floor((nrow - t_out - P.a3max) * (1.0 / 33554432.0)) - 2.0;
+          r_out = (int)fmin(fmax(v, -2147483000.0), 2147483000.0);
+        }
+        my_c[lane] = (int32_t)(P.nq[pb + col0 + lane] >> 25);
         const bool col_ok_lane = col0 + lane < n_k;
         const uint32_t colmask = __ballot_sync(0xffffffffu, col_ok_lane);
         mbar_wait(acc_full + buf, ph_full[buf]);
@@ -363,22 +382,26 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         tmem_ld32(tacc + 2 * kBN, a2);
         tmem_ld_wait();
         __syncwarp();
-        uint32_t in_w = 0, amb_w = 0;
+        uint32_t in_w = 0, out_w = 0;
+        const int4* c4 = reinterpret_cast<const int4*>(my_c);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          // exact in fp64: g = 2^8 (2^8 a0 + a1) + a2  (< 2^40)
-          const int t1 = a0[j] * 256 + a1[j];
-          const double g = fma((double)t1, 256.0, (double)a2[j]);
-          const double d2 = fma(-131072.0, g, nrow + my_ncol[j]);  // D2c + 2^9 a3
-          in_w |= (d2 <= t_in ? 1u : 0u) << j;
-          amb_w |= (d2 <= t_out_fast ? 1u : 0u) << j;
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const int4 cc = c4[j4];
+          const int cj[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = j4 * 4 + jj;
+            const int y = a0[j] * 256 + a1[j] + (a2[j] >> 8) - cj[jj];
+            in_w |= (y >= r_in ? 1u : 0u) << j;
+            out_w |= (y <= r_out ? 1u : 0u) << j;
+          }
         }
         const uint32_t valid = row_ok ? colmask : 0u;
         in_w &= valid;
-        amb_w &= valid & ~in_w;
+        const uint32_t amb_w = valid & ~in_w & ~out_w;
         uint32_t band = 0;
         if (__any_sync(0xffffffffu, amb_w != 0)) {
-          // rare: the omitted A3 term matters -> exact int64 D2c
+          // rare: exact int64 D2c from all four accumulators
           int32_t a3[32];
           tmem_ld32(tacc + 3 * kBN, a3);
           tmem_ld_wait();
@@ -387,8 +410,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
             if (!((amb_w >> j) & 1u)) continue;  // static j keeps a0..a3 in registers
             const int64_t gg = ((int64_t)a0[j] << 32) + ((int64_t)a1[j] << 24) +
                                ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
-            const int64_t d2 = P.nq[pb + gi] + P.nq[pb + col0 + j] - 2 * gg;
-            const double dd = (double)d2;  // exact to 1 ulp; margins cover it
+            const int64_t d2 = nrow_i + P.nq[pb + col0 + j] - 2 * gg;
+            const double dd = (double)d2;  // within 4 units; thresholds carry 64 of margin
             if (dd <= t_in) in_w |= 1u << j;
             else if (dd <= t_out) band |= 1u << j;
           }
@@ -400,23 +423,25 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
         P.adj[tile * kTileWords + row * 4 + half * 2 + ch] = in_w;
         row_count += __popc(in_w);
-        // column counts (off-diagonal tiles only): ballot per column, reduce
-        // the 4 row quarters in smem, one global atomic per column
+        // column counts (off-diagonal tiles only): 32x32 bit transpose across
+        // the warp (lane j then holds column j), popc, reduce the 4 row
+        // quarters in smem, one global atomic per column
         if (J != un.I) {
-          int my = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int c = __popc(__ballot_sync(0xffffffffu, (in_w >> j) & 1u));
-            if (lane == j) my = c;
-          }
+          uint32_t w = in_w;
+          w = bit_transpose_step(w, 16, 0x0000FFFFu, lane);
+          w = bit_transpose_step(w, 8, 0x00FF00FFu, lane);
+          w = bit_transpose_step(w, 4, 0x0F0F0F0Fu, lane);
+          w = bit_transpose_step(w, 2, 0x33333333u, lane);
+          w = bit_transpose_step(w, 1, 0x55555555u, lane);
+          const int my = __popc(w);
           if (my) atomicAdd(colcnt + buf * kBN + ch * 32 + lane, my);
         }
         epi_bar();
         if (J != un.I && q == 0) {
-          int32_t* cc = colcnt + buf * kBN + ch * 32 + lane;
-          const int v = *cc;
+          int32_t* ccp = colcnt + buf * kBN + ch * 32 + lane;
+          const int v = *ccp;
           if (v) atomicAdd(P.cnt + pb + col0 + lane, v);
-          *cc = 0;
+          *ccp = 0;
         }
         buf ^= 1;
         if (band) {

@@ -142,8 +142,15 @@ __host__ __device__ constexpr uint32_t idesc_i8(bool a_signed, bool b_signed) {
          ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 }
 
+struct TileThr {
+  int32_t k_in, k_out;  // integer fast-path offsets (kNever: never certain)
+  double t_in, t_out;   // exact-path thresholds on D2c
+};
+constexpr int32_t kNever = 0x7fffffff;
+
 struct TcParams {
   ElemTables et;
+  const TileThr* thr;     // per bitmap tile pair
   const Unit* units;
   int64_t n_units;
   const int64_t* nq;      // per padded row: sum q^2
@@ -177,6 +184,30 @@ __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI,
   t_in = ri > 0.0 ? ri * ri * (1.0 - 1e-12) - 64.0 : -kBig;
   const double ro = P.a_out[k] + du;
   t_out = ro * ro * (1.0 + 1e-12) + P.ll2 + 64.0;
+}
+
+// Per bitmap tile pair: exact thresholds t_in/t_out on D2c and the integer
+// offsets of the fast path (see the epilogue): with ni25 = floor(N_i/2^25),
+//   r_in  = ni25 + ceil(-t_in/2^25) + 3   >= (N_i - t_in)/2^25 + 2
+//   r_out = ni25 + floor(-(t_out + a3max)/2^25) - 2 <= (N_i - t_out - a3max)/2^25 - 1
+__global__ void tile_thr_kernel(TcParams P, int64_t n_tp, TileThr* __restrict__ out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_tp) return;
+  int k, I, J;
+  decode_tile(P.et, g, k, I, J);
+  double t_in, t_out;
+  thresholds(P, k, P.tbase[k] + I, P.tbase[k] + J, t_in, t_out);
+  TileThr th;
+  th.t_in = t_in;
+  th.t_out = t_out;
+  const double sc = 1.0 / 33554432.0;
+  th.k_in = t_in > -1e18 ? (int32_t)fmin(fmax(ceil(-t_in * sc) + 3.0, -1073741824.0), 1073741824.0)
+                         : kNever;
+  // clamping k_in down is conservative (fewer certain-inside pairs); k_out
+  // must never be raised, so out-of-range values disable the certain-outside test
+  const double ko = floor(-(t_out + P.a3max) * sc) - 2.0;
+  th.k_out = (t_out < 1e18 && ko >= -1073741824.0) ? (int32_t)ko : kNever;
+  out[g] = th;
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
@@ -348,27 +379,21 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
       const int64_t nrow_i = P.nq[pb + gi];
-      const double nrow = (double)nrow_i;
+      const int ni25 = (int)(nrow_i >> 25);
       const int64_t tI = P.tbase[k] + un.I;
       int row_count = 0;
       for (int b = un.b0; b < un.b1; ++b) {
         const int J = b >> 1, half = b & 1;
         const int col0 = b * kBN + ch * 32;           // first local column of this warp
-        double t_in, t_out;
-        thresholds(P, k, tI, P.tbase[k] + J, t_in, t_out);
         // Integer fast path. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
         //   y >= r_in  => D2c <= t_in (certainly inside)
         //   y <= r_out => D2c >  t_out (certainly outside, A3 and L.L bounded)
-        // (derivation in DESIGN.md; +-1 margins absorb every rounding).
-        int r_in = 0x7fffffff, r_out = (int)0x80000000;
-        if (t_in > -1e18) {
-          const double v = ceil((nrow - t_in) * (1.0 / 33554432.0)) + 2.0;
-          r_in = (int)fmin(fmax(v, -2147483000.0), 2147483000.0);
-        }
-        if (t_out < 1e18) {
-          const double v = floor((nrow - t_out - P.a3max) * (1.0 / 33554432.0)) - 2.0;
-          r_out = (int)fmin(fmax(v, -2147483000.0), 2147483000.0);
-        }
+        // r = floor(N_i/2^25) + per-tile constant (tile_thr_kernel; the
+        // constants carry the margins that absorb every rounding).
+        const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
+        const TileThr th = P.thr[tile];
+        const int r_in = th.k_in == kNever ? 0x7fffffff : ni25 + th.k_in;
+        const int r_out = th.k_out == kNever ? (int)0x80000000 : ni25 + th.k_out;
         my_c[lane] = (int32_t)(P.nq[pb + col0 + lane] >> 25);
         const bool col_ok_lane = col0 + lane < n_k;
         const uint32_t colmask = __ballot_sync(0xffffffffu, col_ok_lane);
@@ -412,15 +437,14 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
                                ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
             const int64_t d2 = nrow_i + P.nq[pb + col0 + j] - 2 * gg;
             const double dd = (double)d2;  // within 4 units; thresholds carry 64 of margin
-            if (dd <= t_in) in_w |= 1u << j;
-            else if (dd <= t_out) band |= 1u << j;
+            if (dd <= th.t_in) in_w |= 1u << j;
+            else if (dd <= th.t_out) band |= 1u << j;
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + buf);
         // bitmap word (row, 32 columns) of tile (I, J)
-        const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
         P.adj[tile * kTileWords + row * 4 + half * 2 + ch] = in_w;
         row_count += __popc(in_w);
         // column counts (off-diagonal tiles only): 32x32 bit transpose across
@@ -761,6 +785,8 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
                            stream>>>(s_te.as<unsigned long long>(), d_tile_elem, n_tiles, scale,
                                      n_el, eps, gamma, tile_u, a_in, a_out);
   BM_CHECK_LAUNCH();
+  Scratch s_tt;
+  BM_TRY(scratch_alloc(s_tt, (size_t)n_tp * sizeof(TileThr), stream));
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
     BM_TRY(scratch_alloc(s_q, qcap * sizeof(int2), stream));
@@ -783,6 +809,12 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     prm.queue = s_q.as<int2>();
     prm.qcount = d_cnt;
     prm.qcap = qcap;
+    prm.thr = s_tt.as<TileThr>();
+    if (attempt == 0) {
+      tile_thr_kernel<<<(unsigned)ceil_div(n_tp, 256), 256, 0, stream>>>(prm, n_tp,
+                                                                         s_tt.as<TileThr>());
+      BM_CHECK_LAUNCH();
+    }
     const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
     tc_adjacency_kernel<<<grid, kThreads, smem, stream>>>(qmap, prm);
     BM_CHECK_LAUNCH();

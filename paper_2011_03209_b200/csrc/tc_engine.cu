@@ -46,12 +46,13 @@ int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64
 namespace {
 
 constexpr int kBM = 128;        // A rows (TMEM lanes)
-constexpr int kBN = 64;         // B rows per tile (MMA N)
+constexpr int kBN = 128;        // B rows per tile (MMA N)
 constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
-constexpr int kStages = 2;      // B ring depth
-constexpr int kUnitB = 32;      // B tiles per work unit (<= 16 bitmap tiles)
+constexpr int kStages = 2;      // B ring depth (full-K B tiles)
+constexpr int kUnitB = 16;      // B (= bitmap) tiles per work unit
 constexpr int kEpiWarps = 8;    // epilogue warps 4..11
-constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kLoadWarps = 4;   // A-loader warps 12..15
+constexpr int kThreads = 128 + 32 * (kEpiWarps + kLoadWarps);
 constexpr int kQBits = 23;      // |q| <= 2^23 - 1
 
 struct Unit {
@@ -108,9 +109,9 @@ __device__ __forceinline__ void tc_commit(uint64_t* b) {
           smem_u32(b))
       : "memory");
 }
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8, s32 accumulate
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t idesc, uint32_t accumulate) {
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (both operands in shared memory)
+__device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -164,6 +165,8 @@ struct TcParams {
   uint32_t* adj;
   int32_t* cnt;           // eps-neighbour counts per padded row (self included)
   int2* queue;
+  const uint8_t* planes;  // limb planes [3][P][kpad]
+  int64_t P;
   unsigned long long* qcount;
   unsigned long long qcap;
 };
@@ -233,31 +236,78 @@ __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
 }
 
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A from tensor memory)
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+// Warp roles (512 threads): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator,
+// 4..11 epilogue, 12..15 A loaders (TMEM lane quarter = warp % 4).
+// TMEM columns: [0, kpad/2) A limb planes H|M (row = lane, 4 int8 of K per
+// column); [128, 512) accumulators A0 | A1 | A2 (N = 128 columns each).
+// Shared memory: A limb plane L (SW128 K-major, resident per unit) and a
+// 2-stage ring of full-K B tiles (3 limb planes x 128 rows).
 __global__ void __launch_bounds__(kThreads, 1)
 tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // the SW128 operand tiles need 1024-byte alignment; the dynamic window starts
+  // after the 1 KB reserved block, which is 1024-aligned (checked, not assumed)
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  uint8_t* smem = smem_raw;
   const int nkc = P.nkc;
-  const uint32_t a_plane_bytes = (uint32_t)nkc * kBM * kKC;   // per limb plane
-  const uint32_t b_plane_bytes = (uint32_t)nkc * kBN * kKC;
-  const uint32_t a_bytes = 3 * a_plane_bytes;
+  const int kpad = nkc * kKC;
+  const uint32_t blk = (uint32_t)kBN * kKC;            // one (plane, K-chunk) block: 16 KB
+  const uint32_t aL_bytes = (uint32_t)nkc * blk;
+  const uint32_t b_plane_bytes = (uint32_t)nkc * blk;
   const uint32_t b_bytes = 3 * b_plane_bytes;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + a_bytes;
+  uint8_t* sAL = smem;
+  uint8_t* sB = smem + aL_bytes;
   uint64_t* bars = (uint64_t*)(sB + kStages * b_bytes);
-  uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 1;
-  uint64_t* b_full = bars + 2;                // [kStages]
+  uint64_t* a_tm_full = bars + 0;             // H/M planes stored to TMEM (4 loader warps)
+  uint64_t* a_sm_full = bars + 1;             // L plane landed in smem (TMA tx)
+  uint64_t* a_empty = bars + 2;               // MMAs of the unit done
+  uint64_t* b_full = bars + 3;                // [kStages]
   uint64_t* b_empty = b_full + kStages;       // [kStages]
-  uint64_t* acc_full = b_empty + kStages;     // [2]
+  uint64_t* acc_full = b_empty + kStages;     // [2]: (A0, A1), A2
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
   int32_t* colcnt = (int32_t*)(tmem_slot + 4);            // [2][kBN]
-  double* ncol = (double*)(colcnt + 2 * kBN);             // [kEpiWarps][32]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(a_full, 1);
+    mbar_init(a_tm_full, kLoadWarps);
+    mbar_init(a_sm_full, 1);
     mbar_init(a_empty, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(b_full + s, 1);
@@ -279,23 +329,24 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tacc0 = tmem_base + 128;  // accumulator columns
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ producer (TMA)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qmap) : "memory");
-      uint32_t a_empty_ph = 0, stage = 0, ph_empty[kStages] = {0, 0};
+      uint32_t stage = 0, ph_empty[kStages] = {0, 0}, a_empty_ph = 0;
       for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
         const Unit un = P.units[u];
         const int pb = P.et.pbase[un.k];
+        // A limb plane L of row tile I (resident for the unit)
         mbar_wait(a_empty, a_empty_ph ^ 1);
         a_empty_ph ^= 1;
-        mbar_expect_tx(a_full, a_bytes);
-        for (int pl = 0; pl < 3; ++pl)
-          for (int c = 0; c < nkc; ++c)
-            for (int h = 0; h < 2; ++h)
-              tma_load_3d(sA + pl * a_plane_bytes + (c * kBM + h * 64) * kKC, &qmap, a_full,
-                          c * kKC, pb + un.I * kBM + h * 64, pl);
+        mbar_expect_tx(a_sm_full, aL_bytes);
+        for (int c = 0; c < nkc; ++c)
+          for (int h = 0; h < 2; ++h)
+            tma_load_3d(sAL + c * blk + h * 64 * kKC, &qmap, a_sm_full, c * kKC,
+                        pb + un.I * kBM + h * 64, 2);
         for (int b = un.b0; b < un.b1; ++b) {
           mbar_wait(b_empty + stage, ph_empty[stage] ^ 1);
           ph_empty[stage] ^= 1;
@@ -303,8 +354,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           uint8_t* dst = sB + stage * b_bytes;
           for (int pl = 0; pl < 3; ++pl)
             for (int c = 0; c < nkc; ++c)
-              tma_load_3d(dst + pl * b_plane_bytes + c * kBN * kKC, &qmap, b_full + stage,
-                          c * kKC, pb + b * kBN, pl);
+              for (int h = 0; h < 2; ++h)
+                tma_load_3d(dst + pl * b_plane_bytes + c * blk + h * 64 * kKC, &qmap,
+                            b_full + stage, c * kKC, pb + b * kBN + h * 64, pl);
           stage = (stage + 1) % kStages;
         }
       }
@@ -316,60 +368,104 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       constexpr uint32_t ID_SU = idesc_i8(true, false);
       constexpr uint32_t ID_US = idesc_i8(false, true);
       constexpr uint32_t ID_UU = idesc_i8(false, false);
-      uint32_t a_full_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
-      uint32_t buf = 0, ph_acc_empty[2] = {0, 0};
-      const uint32_t sA_addr = smem_u32(sA);
+      uint32_t a_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
+      uint32_t ph_acc[2] = {0, 0};
+      const uint32_t ncol_plane = (uint32_t)kpad / 4;   // TMEM columns per limb plane
+      const uint32_t aH = tmem_base, aM = tmem_base + ncol_plane;
+      const uint32_t sAL_addr = smem_u32(sAL);
+      const int ksteps = kpad / 32;
       for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
         const Unit un = P.units[u];
-        mbar_wait(a_full, a_full_ph);
-        a_full_ph ^= 1;
+        mbar_wait(a_tm_full, a_ph);
+        mbar_wait(a_sm_full, a_ph);
+        a_ph ^= 1;
         tc_fence_after();
         for (int b = un.b0; b < un.b1; ++b) {
           mbar_wait(b_full + stage, ph_full[stage]);
           ph_full[stage] ^= 1;
-          mbar_wait(acc_empty + buf, ph_acc_empty[buf] ^ 1);
-          ph_acc_empty[buf] ^= 1;
-          tc_fence_after();
           const uint32_t sB_addr = smem_u32(sB + stage * b_bytes);
-          const uint32_t acc = tmem_base + buf * 4 * kBN;
-          for (int c = 0; c < nkc; ++c) {
-            for (int kk = 0; kk < kKC / 32; ++kk) {
-              const uint32_t off = c * kBM * kKC + kk * 32;
-              const uint32_t offb = c * kBN * kKC + kk * 32;
-              const uint64_t aH = smem_desc(sA_addr + 0 * a_plane_bytes + off);
-              const uint64_t aM = smem_desc(sA_addr + 1 * a_plane_bytes + off);
-              const uint64_t aL = smem_desc(sA_addr + 2 * a_plane_bytes + off);
-              const uint64_t bH = smem_desc(sB_addr + 0 * b_plane_bytes + offb);
-              const uint64_t bM = smem_desc(sB_addr + 1 * b_plane_bytes + offb);
-              const uint64_t bL = smem_desc(sB_addr + 2 * b_plane_bytes + offb);
-              const uint32_t first = (c == 0 && kk == 0) ? 0u : 1u;
-              mma_i8(acc + 0 * kBN, aH, bH, ID_SS, first);
-              mma_i8(acc + 1 * kBN, aH, bM, ID_SU, first);
-              mma_i8(acc + 1 * kBN, aM, bH, ID_US, 1u);
-              mma_i8(acc + 2 * kBN, aH, bL, ID_SU, first);
-              mma_i8(acc + 2 * kBN, aM, bM, ID_UU, 1u);
-              mma_i8(acc + 2 * kBN, aL, bH, ID_US, 1u);
-              mma_i8(acc + 3 * kBN, aM, bL, ID_UU, first);
-              mma_i8(acc + 3 * kBN, aL, bM, ID_UU, 1u);
-            }
+          auto bdesc = [&](int pl, int ks) {
+            return smem_desc(sB_addr + pl * b_plane_bytes + (ks >> 2) * blk + (ks & 3) * 32);
+          };
+          // phase 1 — shift classes 2^32, 2^24: A0 = H.H, A1 = H.M + M.H
+          mbar_wait(acc_empty + 0, ph_acc[0] ^ 1);
+          tc_fence_after();
+          for (int ks = 0; ks < ksteps; ++ks) {
+            mma_i8_ts(tacc0 + 0 * kBN, aH + ks * 8, bdesc(0, ks), ID_SS, ks > 0);
+            mma_i8_ts(tacc0 + 1 * kBN, aH + ks * 8, bdesc(1, ks), ID_SU, ks > 0);
+            mma_i8_ts(tacc0 + 1 * kBN, aM + ks * 8, bdesc(0, ks), ID_US, 1u);
           }
+          tc_commit(acc_full + 0);
+          // phase 2 — shift class 2^16: A2 = H.L + M.M + L.H (L of A from smem)
+          mbar_wait(acc_empty + 1, ph_acc[1] ^ 1);
+          tc_fence_after();
+          for (int ks = 0; ks < ksteps; ++ks) {
+            mma_i8_ts(tacc0 + 2 * kBN, aH + ks * 8, bdesc(2, ks), ID_SU, ks > 0);
+            mma_i8_ts(tacc0 + 2 * kBN, aM + ks * 8, bdesc(1, ks), ID_UU, 1u);
+            mma_i8_ss(tacc0 + 2 * kBN, smem_desc(sAL_addr + (ks >> 2) * blk + (ks & 3) * 32),
+                      bdesc(0, ks), ID_US, 1u);
+          }
+          tc_commit(acc_full + 1);
           tc_commit(b_empty + stage);   // B slot reusable once these MMAs finish
-          tc_commit(acc_full + buf);    // accumulators ready for the epilogue
+          ph_acc[0] ^= 1;
+          ph_acc[1] ^= 1;
           stage = (stage + 1) % kStages;
-          buf ^= 1;
         }
-        tc_commit(a_empty);             // A tile reusable
+        tc_commit(a_empty);             // A planes reusable
+      }
+    }
+  } else if (warp >= 4 + kEpiWarps) {
+    // ------------------------------------------------------------ A loaders (H, M -> TMEM)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t ncol_plane = (uint32_t)kpad / 4;
+    uint32_t a_empty_ph = 0;
+    for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+      const Unit un = P.units[u];
+      const int64_t prow = (int64_t)P.et.pbase[un.k] + un.I * kBM + row;
+      mbar_wait(a_empty, a_empty_ph ^ 1);
+      a_empty_ph ^= 1;
+      tc_fence_after();
+      for (int pl = 0; pl < 2; ++pl) {
+        const uint4* src = reinterpret_cast<const uint4*>(P.planes + (int64_t)pl * P.P * kpad +
+                                                           prow * kpad);
+        for (int c0 = 0; c0 < kpad / 4; c0 += 32) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint4 w = __ldg(src + c0 / 4 + i);
+            v[4 * i] = w.x;
+            v[4 * i + 1] = w.y;
+            v[4 * i + 2] = w.z;
+            v[4 * i + 3] = w.w;
+          }
+          tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + pl * ncol_plane + c0, v);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_tm_full);
+      // warm L2 with the next unit's A rows
+      const int64_t un_next = u + gridDim.x;
+      if (un_next < P.n_units) {
+        const Unit nx = P.units[un_next];
+        const int64_t nrow = (int64_t)P.et.pbase[nx.k] + nx.I * kBM + row;
+        for (int pl = 0; pl < 2; ++pl)
+          for (int off = 0; off < kpad; off += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.planes + (int64_t)pl * P.P * kpad +
+                                                          nrow * kpad + off));
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    // warp (q, ch): TMEM lane quarter q (rows 32q..32q+31), column half ch
+    // warp (q, ch): TMEM lane quarter q (rows 32q..32q+31), column half ch (64 columns)
     const int ew = warp - 4;
     const int q = warp & 3;            // tcgen05.ld lane window = warp % 4
     const int ch = ew >> 2;
     const int row = q * 32 + lane;
-    int32_t* my_c = reinterpret_cast<int32_t*>(ncol) + ew * 32;  // floor(N_j / 2^25)
-    uint32_t buf = 0, ph_full[2] = {0, 0};
+    uint32_t ph_acc[2] = {0, 0};
+    uint32_t cbank = 0;                // colcnt double buffer
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
       const Unit un = P.units[u];
       const int k = un.k;
@@ -378,104 +474,116 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const int64_t T = P.et.ntiles[k];
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
-      const int64_t nrow_i = P.nq[pb + gi];
-      const int ni25 = (int)(nrow_i >> 25);
-      const int64_t tI = P.tbase[k] + un.I;
+      const int ni25 = (int)(P.nq[pb + gi] >> 25);
       int row_count = 0;
-      for (int b = un.b0; b < un.b1; ++b) {
-        const int J = b >> 1, half = b & 1;
-        const int col0 = b * kBN + ch * 32;           // first local column of this warp
-        // Integer fast path. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
-        //   y >= r_in  => D2c <= t_in (certainly inside)
-        //   y <= r_out => D2c >  t_out (certainly outside, A3 and L.L bounded)
-        // r = floor(N_i/2^25) + per-tile constant (tile_thr_kernel; the
-        // constants carry the margins that absorb every rounding).
+      for (int J = un.b0; J < un.b1; ++J) {
+        const int col0 = J * kBN + ch * 64;           // first local column of this warp
+        // Integer decision. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
+        //   y >= r_in  => D2c <= t_in (certainly inside; a3, L.L >= 0)
+        //   y <= r_out => D2c >  t_out (certainly outside; a3, L.L bounded)
+        //   otherwise  => exact fp64 recheck in the element's order
+        // r = floor(N_i/2^25) + per-tile constant (tile_thr_kernel, with the
+        // margins that absorb every rounding).
         const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
         const TileThr th = P.thr[tile];
         const int r_in = th.k_in == kNever ? 0x7fffffff : ni25 + th.k_in;
         const int r_out = th.k_out == kNever ? (int)0x80000000 : ni25 + th.k_out;
-        my_c[lane] = (int32_t)(P.nq[pb + col0 + lane] >> 25);
-        const bool col_ok_lane = col0 + lane < n_k;
-        const uint32_t colmask = __ballot_sync(0xffffffffu, col_ok_lane);
-        mbar_wait(acc_full + buf, ph_full[buf]);
-        ph_full[buf] ^= 1;
+        // floor(N_j / 2^25) of this warp's 64 columns: lane j holds columns j, 32 + j
+        const int cown0 = (int)(P.nq[pb + col0 + lane] >> 25);
+        const int cown1 = (int)(P.nq[pb + col0 + 32 + lane] >> 25);
+        const uint32_t colmask0 = __ballot_sync(0xffffffffu, col0 + lane < n_k);
+        const uint32_t colmask1 = __ballot_sync(0xffffffffu, col0 + 32 + lane < n_k);
+        const uint32_t tq = tacc0 + ((uint32_t)(q * 32) << 16) + ch * 64;
+        // --- phase 1: t1 = 256 a0 + a1 (exact int32), then release A0/A1
+        mbar_wait(acc_full + 0, ph_acc[0]);
         tc_fence_after();
-        const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + buf * 4 * kBN + ch * 32;
-        int32_t a0[32], a1[32], a2[32];
-        tmem_ld32(tacc + 0 * kBN, a0);
-        tmem_ld32(tacc + 1 * kBN, a1);
-        tmem_ld32(tacc + 2 * kBN, a2);
-        tmem_ld_wait();
-        __syncwarp();
-        uint32_t in_w = 0, out_w = 0;
-        const int4* c4 = reinterpret_cast<const int4*>(my_c);
+        int32_t t1[64];
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const int4 cc = c4[j4];
-          const int cj[4] = {cc.x, cc.y, cc.z, cc.w};
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = j4 * 4 + jj;
-            const int y = a0[j] * 256 + a1[j] + (a2[j] >> 8) - cj[jj];
-            in_w |= (y >= r_in ? 1u : 0u) << j;
-            out_w |= (y <= r_out ? 1u : 0u) << j;
-          }
-        }
-        const uint32_t valid = row_ok ? colmask : 0u;
-        in_w &= valid;
-        const uint32_t amb_w = valid & ~in_w & ~out_w;
-        uint32_t band = 0;
-        if (__any_sync(0xffffffffu, amb_w != 0)) {
-          // rare: exact int64 D2c from all four accumulators
-          int32_t a3[32];
-          tmem_ld32(tacc + 3 * kBN, a3);
+        for (int h = 0; h < 4; ++h) {
+          int32_t x0[16], x1[16];
+          tmem_ld16(tq + 0 * kBN + h * 16, x0);
+          tmem_ld16(tq + 1 * kBN + h * 16, x1);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (!((amb_w >> j) & 1u)) continue;  // static j keeps a0..a3 in registers
-            const int64_t gg = ((int64_t)a0[j] << 32) + ((int64_t)a1[j] << 24) +
-                               ((int64_t)a2[j] << 16) + ((int64_t)a3[j] << 8);
-            const int64_t d2 = nrow_i + P.nq[pb + col0 + j] - 2 * gg;
-            const double dd = (double)d2;  // within 4 units; thresholds carry 64 of margin
-            if (dd <= th.t_in) in_w |= 1u << j;
-            else if (dd <= th.t_out) band |= 1u << j;
-          }
+          for (int j = 0; j < 16; ++j) t1[h * 16 + j] = x0[j] * 256 + x1[j];
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty + buf);
-        // bitmap word (row, 32 columns) of tile (I, J)
-        P.adj[tile * kTileWords + row * 4 + half * 2 + ch] = in_w;
-        row_count += __popc(in_w);
-        // column counts (off-diagonal tiles only): 32x32 bit transpose across
+        if (lane == 0) mbar_arrive(acc_empty + 0);
+        // --- phase 2: decisions from A2
+        mbar_wait(acc_full + 1, ph_acc[1]);
+        tc_fence_after();
+        uint32_t in_w[2] = {0u, 0u}, amb_w[2] = {0u, 0u};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          int32_t a2[16];
+          tmem_ld16(tq + 2 * kBN + h * 16, a2);
+          tmem_ld_wait();
+          uint32_t iw = 0, ow = 0;
+          const int cown = (h < 2) ? cown0 : cown1;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int cj = __shfl_sync(0xffffffffu, cown, (h & 1) * 16 + j);
+            const int y = t1[h * 16 + j] + (a2[j] >> 8) - cj;
+            iw |= (y >= r_in ? 1u : 0u) << j;
+            ow |= (y <= r_out ? 1u : 0u) << j;
+          }
+          const int sh = (h & 1) * 16;
+          in_w[h >> 1] |= iw << sh;
+          amb_w[h >> 1] |= (~iw & ~ow & 0xffffu) << sh;
+        }
+        in_w[0] &= row_ok ? colmask0 : 0u;
+        in_w[1] &= row_ok ? colmask1 : 0u;
+        amb_w[0] &= row_ok ? colmask0 : 0u;
+        amb_w[1] &= row_ok ? colmask1 : 0u;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + 1);
+        ph_acc[0] ^= 1;
+        ph_acc[1] ^= 1;
+        // bitmap words (row, 2 x 32 columns) of tile (I, J)
+        *reinterpret_cast<uint2*>(P.adj + tile * kTileWords + row * 4 + ch * 2) =
+            make_uint2(in_w[0], in_w[1]);
+        row_count += __popc(in_w[0]) + __popc(in_w[1]);
+        // column counts (off-diagonal tiles only): 32x32 bit transposes across
         // the warp (lane j then holds column j), popc, reduce the 4 row
         // quarters in smem, one global atomic per column
         if (J != un.I) {
-          uint32_t w = in_w;
-          w = bit_transpose_step(w, 16, 0x0000FFFFu, lane);
-          w = bit_transpose_step(w, 8, 0x00FF00FFu, lane);
-          w = bit_transpose_step(w, 4, 0x0F0F0F0Fu, lane);
-          w = bit_transpose_step(w, 2, 0x33333333u, lane);
-          w = bit_transpose_step(w, 1, 0x55555555u, lane);
-          const int my = __popc(w);
-          if (my) atomicAdd(colcnt + buf * kBN + ch * 32 + lane, my);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t w = in_w[h];
+            w = bit_transpose_step(w, 16, 0x0000FFFFu, lane);
+            w = bit_transpose_step(w, 8, 0x00FF00FFu, lane);
+            w = bit_transpose_step(w, 4, 0x0F0F0F0Fu, lane);
+            w = bit_transpose_step(w, 2, 0x33333333u, lane);
+            w = bit_transpose_step(w, 1, 0x55555555u, lane);
+            const int my = __popc(w);
+            if (my) atomicAdd(colcnt + cbank * kBN + ch * 64 + h * 32 + lane, my);
+          }
         }
         epi_bar();
         if (J != un.I && q == 0) {
-          int32_t* ccp = colcnt + buf * kBN + ch * 32 + lane;
-          const int v = *ccp;
-          if (v) atomicAdd(P.cnt + pb + col0 + lane, v);
-          *ccp = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int32_t* ccp = colcnt + cbank * kBN + ch * 64 + h * 32 + lane;
+            const int v = *ccp;
+            if (v) atomicAdd(P.cnt + pb + col0 + h * 32 + lane, v);
+            *ccp = 0;
+          }
         }
-        buf ^= 1;
-        if (band) {
-          const unsigned long long nb = __popc(band);
-          unsigned long long i = atomicAdd(P.qcount, nb);
-          while (band) {
-            const int j = __ffs(band) - 1;
-            band &= band - 1;
-            if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + j);
-            ++i;
+        cbank ^= 1;
+        // undecided pairs -> exact recheck queue
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t band = amb_w[h];
+          if (band) {
+            unsigned long long i = atomicAdd(P.qcount, (unsigned long long)__popc(band));
+            while (band) {
+              const int j = __ffs(band) - 1;
+              band &= band - 1;
+              if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + h * 32 + j);
+              ++i;
+            }
           }
         }
       }
@@ -489,6 +597,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // preparation: per-element centre / scale, quantisation, per-tile error max
@@ -718,9 +827,9 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     tbase[k + 1] = (int32_t)(tbase[k] + T);
     for (int64_t t = 0; t < T; ++t) tile_elem[tbase[k] + t] = (int32_t)k;
     for (int64_t I = 0; I < T; ++I)
-      for (int64_t b0 = 2 * I; b0 < 2 * T; b0 += kUnitB)
+      for (int64_t b0 = I; b0 < T; b0 += kUnitB)
         units.push_back({(int32_t)k, (int32_t)I, (int32_t)b0,
-                         (int32_t)std::min<int64_t>(b0 + kUnitB, 2 * T)});
+                         (int32_t)std::min<int64_t>(b0 + kUnitB, T)});
   }
   const int64_t n_units = (int64_t)units.size();
   if (n_units == 0) return BM_OK;
@@ -768,7 +877,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   unsigned long long qcap = std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 5000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
-  const size_t smem = 1024 + 3 * (size_t)nkc * kKC * (kBM + kStages * kBN) + 256 + 4096;
+  const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024;
   static bool attr = false;
   if (!attr) {
     BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel,
@@ -807,6 +916,8 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     prm.adj = adj;
     prm.cnt = cnt;
     prm.queue = s_q.as<int2>();
+    prm.planes = s_pl.as<uint8_t>();
+    prm.P = P;
     prm.qcount = d_cnt;
     prm.qcap = qcap;
     prm.thr = s_tt.as<TileThr>();

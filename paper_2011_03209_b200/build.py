@@ -41,7 +41,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
     tmp = OUT + ".tmp"
-    cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, *sources()]
+    extra = os.environ.get("B200MAP_NVCC_FLAGS", "").split()  # e.g. -DBM_TC_PROFILE
+    cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, *sources()]
     if verbose:
         print(" ".join(cmd))
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -33,6 +33,9 @@
 // so the epilogue of tile b overlaps the MMAs of tile b+1.
 #include <cuda.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -49,11 +52,12 @@ constexpr int kBM = 128;        // A rows (TMEM lanes)
 constexpr int kBN = 128;        // B rows per tile (MMA N)
 constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
 constexpr int kStages = 2;      // B ring depth (full-K B tiles)
-constexpr int kUnitB = 16;      // B (= bitmap) tiles per work unit
+constexpr int kUnitB = 32;      // B (= bitmap) tiles per work unit
+constexpr int kInfo = 3;        // per-tile info ring depth (smem)
 constexpr int kEpiWarps = 8;    // epilogue warps 4..11
 constexpr int kLoadWarps = 4;   // A-loader warps 12..15
 constexpr int kThreads = 128 + 32 * (kEpiWarps + kLoadWarps);
-constexpr int kQBits = 23;      // |q| <= 2^23 - 1
+constexpr int kQBits = 22;      // |q| <= 2^22 - 1 (H in [-64, 63]: every y below fits in int32)
 
 struct Unit {
   int32_t k, I, b0, b1;
@@ -97,28 +101,52 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(b))
-      : "memory");
-}
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (both operands in shared memory)
-__device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
+// One elected lane of a converged warp issues; operands stay warp-uniform.
+__device__ __forceinline__ void mma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
-      ".reg .pred p;\n"
+      ".reg .pred p, e;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ss_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* b) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(b))
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() {
@@ -148,6 +176,14 @@ struct TileThr {
   double t_in, t_out;   // exact-path thresholds on D2c
 };
 constexpr int32_t kNever = 0x7fffffff;
+#ifdef BM_TC_PROFILE
+#define EP_START() long long te = clock64()
+#define EP_MARK(i) (ep[i] += clock64() - te, te = clock64())
+#else
+#define EP_START() ((void)0)
+#define EP_MARK(i) ((void)0)
+#endif
+constexpr int kYMax = 500000000;  // bound on |y| (kQBits = 22, Kpad <= 256)
 
 struct TcParams {
   ElemTables et;
@@ -155,6 +191,7 @@ struct TcParams {
   const Unit* units;
   int64_t n_units;
   const int64_t* nq;      // per padded row: sum q^2
+  const int32_t* cq;      // per padded row: floor(sum q^2 / 2^25)
   const double* tile_u;   // per 128-row tile: max quantisation error / s_k (quantised units)
   const int32_t* tbase;   // per element: first global 128-row tile index
   const double* a_in;     // per element: eps / (1 + gamma) / s_k
@@ -169,6 +206,7 @@ struct TcParams {
   int64_t P;
   unsigned long long* qcount;
   unsigned long long qcap;
+  long long* prof;        // optional [grid][8] cycle counters of the MMA warp (B200MAP_TC_PROFILE)
 };
 
 constexpr double kBig = 4.0e18;
@@ -213,19 +251,6 @@ __global__ void tile_thr_kernel(TcParams P, int64_t n_tp, TileThr* __restrict__ 
   out[g] = th;
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-        "=r"(v[31])
-      : "r"(taddr));
-}
-
 // one step of the in-warp 32x32 bit-matrix transpose (lane i holds row i)
 __device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32_t m, int lane) {
   const uint32_t t = __shfl_xor_sync(0xffffffffu, w, s);
@@ -234,19 +259,6 @@ __device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32
 
 __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-}
-
-// D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A from tensor memory)
-__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
@@ -278,6 +290,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 // column); [128, 512) accumulators A0 | A1 | A2 (N = 128 columns each).
 // Shared memory: A limb plane L (SW128 K-major, resident per unit) and a
 // 2-stage ring of full-K B tiles (3 limb planes x 128 rows).
+template <int NKC>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -285,8 +298,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   // after the 1 KB reserved block, which is 1024-aligned (checked, not assumed)
   if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
   uint8_t* smem = smem_raw;
-  const int nkc = P.nkc;
-  const int kpad = nkc * kKC;
+  constexpr int nkc = NKC;
+  constexpr int kpad = nkc * kKC;
   const uint32_t blk = (uint32_t)kBN * kKC;            // one (plane, K-chunk) block: 16 KB
   const uint32_t aL_bytes = (uint32_t)nkc * blk;
   const uint32_t b_plane_bytes = (uint32_t)nkc * blk;
@@ -303,6 +316,16 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
   int32_t* colcnt = (int32_t*)(tmem_slot + 4);            // [2][kBN]
+  // per-tile info ring, filled ahead by the producer: floor(N_j/2^25) of the
+  // tile's 128 columns (bulk TMA) + the tile's integer threshold offsets
+  struct TileInfo {
+    int32_t cq[kBN];
+    int2 th;
+    int2 pad;
+  };
+  TileInfo* info = (TileInfo*)(((uintptr_t)(colcnt + 2 * kBN) + 15) & ~(uintptr_t)15);
+  uint64_t* info_full = (uint64_t*)(info + kInfo);        // [kInfo]
+  uint64_t* info_empty = info_full + kInfo;               // [kInfo]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -316,6 +339,10 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kEpiWarps);
+    }
+    for (int s = 0; s < kInfo; ++s) {
+      mbar_init(info_full + s, 1);
+      mbar_init(info_empty + s, kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -336,10 +363,13 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qmap) : "memory");
       uint32_t stage = 0, ph_empty[kStages] = {0, 0}, a_empty_ph = 0;
+      uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
       for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
         const Unit un = P.units[u];
         const int pb = P.et.pbase[un.k];
         // A limb plane L of row tile I (resident for the unit)
+        const int64_t tpk = P.et.tp_off[un.k];
+        const int64_t T = P.et.ntiles[un.k];
         mbar_wait(a_empty, a_empty_ph ^ 1);
         a_empty_ph ^= 1;
         mbar_expect_tx(a_sm_full, aL_bytes);
@@ -348,6 +378,13 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
             tma_load_3d(sAL + c * blk + h * 64 * kKC, &qmap, a_sm_full, c * kKC,
                         pb + un.I * kBM + h * 64, 2);
         for (int b = un.b0; b < un.b1; ++b) {
+          // tile info for the epilogue (runs ahead by up to kInfo tiles)
+          mbar_wait(info_empty + islot, ph_info[islot] ^ 1);
+          ph_info[islot] ^= 1;
+          info[islot].th = *reinterpret_cast<const int2*>(P.thr + tpk + tri_index(un.I, b, T));
+          mbar_expect_tx(info_full + islot, kBN * 4);
+          bulk_load(info[islot].cq, P.cq + pb + b * kBN, kBN * 4, info_full + islot);
+          islot = (islot + 1) % kInfo;
           mbar_wait(b_empty + stage, ph_empty[stage] ^ 1);
           ph_empty[stage] ^= 1;
           mbar_expect_tx(b_full + stage, b_bytes);
@@ -363,56 +400,80 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t ID_SS = idesc_i8(true, true);
-      constexpr uint32_t ID_SU = idesc_i8(true, false);
-      constexpr uint32_t ID_US = idesc_i8(false, true);
-      constexpr uint32_t ID_UU = idesc_i8(false, false);
-      uint32_t a_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
-      uint32_t ph_acc[2] = {0, 0};
-      const uint32_t ncol_plane = (uint32_t)kpad / 4;   // TMEM columns per limb plane
-      const uint32_t aH = tmem_base, aM = tmem_base + ncol_plane;
-      const uint32_t sAL_addr = smem_u32(sAL);
-      const int ksteps = kpad / 32;
-      for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-        const Unit un = P.units[u];
-        mbar_wait(a_tm_full, a_ph);
-        mbar_wait(a_sm_full, a_ph);
-        a_ph ^= 1;
+    // The whole warp runs the loop so every descriptor lives in uniform
+    // registers; one elected lane issues (elect.sync inside the asm).
+    constexpr uint32_t ID_SS = idesc_i8(true, true);
+    constexpr uint32_t ID_SU = idesc_i8(true, false);
+    constexpr uint32_t ID_US = idesc_i8(false, true);
+    constexpr uint32_t ID_UU = idesc_i8(false, false);
+    constexpr int KSTEPS = NKC * 4;
+    constexpr uint32_t NCOL_PLANE = NKC * 32;          // TMEM columns per limb plane
+    constexpr uint32_t BLK = kBN * kKC;                // bytes of one (plane, K-chunk) block
+    constexpr uint32_t BPLANE = NKC * BLK;
+    uint32_t a_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
+    uint32_t ph_acc[2] = {0, 0};
+    const uint32_t aH = tmem_base, aM = tmem_base + NCOL_PLANE;
+    const uint64_t aL_desc = smem_desc(smem_u32(sAL));
+    const uint64_t b_desc0 = smem_desc(smem_u32(sB));
+    long long prof_a = 0, prof_b = 0, prof_e0 = 0, prof_e1 = 0;
+    const long long prof_t0 = clock64();
+    for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+      const Unit un = P.units[u];
+      long long tw = clock64();
+      mbar_wait(a_tm_full, a_ph);
+      mbar_wait(a_sm_full, a_ph);
+      prof_a += clock64() - tw;
+      a_ph ^= 1;
+      tc_fence_after();
+      for (int b = un.b0; b < un.b1; ++b) {
+        tw = clock64();
+        mbar_wait(b_full + stage, ph_full[stage]);
+        prof_b += clock64() - tw;
+        ph_full[stage] ^= 1;
+        const uint64_t bd = b_desc0 + ((stage * 3 * BPLANE) >> 4);
+        // descriptor of (B plane pl, K-step ks): start address advances in 16-byte units
+#define BDESC(pl, ks) (bd + ((uint64_t)((pl) * BPLANE + ((ks) >> 2) * BLK + ((ks) & 3) * 32) >> 4))
+        // phase 1 — shift classes 2^32, 2^24: A0 = H.H, A1 = H.M + M.H
+        tw = clock64();
+        mbar_wait(acc_empty + 0, ph_acc[0] ^ 1);
+        prof_e0 += clock64() - tw;
         tc_fence_after();
-        for (int b = un.b0; b < un.b1; ++b) {
-          mbar_wait(b_full + stage, ph_full[stage]);
-          ph_full[stage] ^= 1;
-          const uint32_t sB_addr = smem_u32(sB + stage * b_bytes);
-          auto bdesc = [&](int pl, int ks) {
-            return smem_desc(sB_addr + pl * b_plane_bytes + (ks >> 2) * blk + (ks & 3) * 32);
-          };
-          // phase 1 — shift classes 2^32, 2^24: A0 = H.H, A1 = H.M + M.H
-          mbar_wait(acc_empty + 0, ph_acc[0] ^ 1);
-          tc_fence_after();
-          for (int ks = 0; ks < ksteps; ++ks) {
-            mma_i8_ts(tacc0 + 0 * kBN, aH + ks * 8, bdesc(0, ks), ID_SS, ks > 0);
-            mma_i8_ts(tacc0 + 1 * kBN, aH + ks * 8, bdesc(1, ks), ID_SU, ks > 0);
-            mma_i8_ts(tacc0 + 1 * kBN, aM + ks * 8, bdesc(0, ks), ID_US, 1u);
-          }
-          tc_commit(acc_full + 0);
-          // phase 2 — shift class 2^16: A2 = H.L + M.M + L.H (L of A from smem)
-          mbar_wait(acc_empty + 1, ph_acc[1] ^ 1);
-          tc_fence_after();
-          for (int ks = 0; ks < ksteps; ++ks) {
-            mma_i8_ts(tacc0 + 2 * kBN, aH + ks * 8, bdesc(2, ks), ID_SU, ks > 0);
-            mma_i8_ts(tacc0 + 2 * kBN, aM + ks * 8, bdesc(1, ks), ID_UU, 1u);
-            mma_i8_ss(tacc0 + 2 * kBN, smem_desc(sAL_addr + (ks >> 2) * blk + (ks & 3) * 32),
-                      bdesc(0, ks), ID_US, 1u);
-          }
-          tc_commit(acc_full + 1);
-          tc_commit(b_empty + stage);   // B slot reusable once these MMAs finish
-          ph_acc[0] ^= 1;
-          ph_acc[1] ^= 1;
-          stage = (stage + 1) % kStages;
+#pragma unroll
+        for (int ks = 0; ks < KSTEPS; ++ks) {
+          mma_ts_elect(tacc0 + 0 * kBN, aH + ks * 8, BDESC(0, ks), ID_SS, ks > 0);
+          mma_ts_elect(tacc0 + 1 * kBN, aH + ks * 8, BDESC(1, ks), ID_SU, ks > 0);
+          mma_ts_elect(tacc0 + 1 * kBN, aM + ks * 8, BDESC(0, ks), ID_US, 1u);
         }
-        tc_commit(a_empty);             // A planes reusable
+        commit_elect(acc_full + 0);
+        // phase 2 — shift class 2^16: A2 = H.L + M.M + L.H (L of A from smem)
+        tw = clock64();
+        mbar_wait(acc_empty + 1, ph_acc[1] ^ 1);
+        prof_e1 += clock64() - tw;
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < KSTEPS; ++ks) {
+          mma_ts_elect(tacc0 + 2 * kBN, aH + ks * 8, BDESC(2, ks), ID_SU, ks > 0);
+          mma_ts_elect(tacc0 + 2 * kBN, aM + ks * 8, BDESC(1, ks), ID_UU, 1u);
+          mma_ss_elect(tacc0 + 2 * kBN,
+                       aL_desc + ((uint64_t)((ks >> 2) * BLK + (ks & 3) * 32) >> 4),
+                       BDESC(0, ks), ID_US, 1u);
+        }
+#undef BDESC
+        commit_elect(acc_full + 1);
+        commit_elect(b_empty + stage);   // B slot reusable once these MMAs finish
+        ph_acc[0] ^= 1;
+        ph_acc[1] ^= 1;
+        stage = (stage + 1) % kStages;
       }
+      commit_elect(a_empty);             // A planes reusable
+    }
+    if (P.prof && lane == 0) {
+      long long* pr = P.prof + blockIdx.x * 8;
+      pr[0] = clock64() - prof_t0;
+      pr[1] = prof_a;
+      pr[2] = prof_b;
+      pr[3] = prof_e0;
+      pr[4] = prof_e1;
     }
   } else if (warp >= 4 + kEpiWarps) {
     // ------------------------------------------------------------ A loaders (H, M -> TMEM)
@@ -466,6 +527,11 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     const int row = q * 32 + lane;
     uint32_t ph_acc[2] = {0, 0};
     uint32_t cbank = 0;                // colcnt double buffer
+    uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
+#ifdef BM_TC_PROFILE
+    long long ep[7] = {0, 0, 0, 0, 0, 0, 0};
+    const long long ep_t0 = clock64();
+#endif
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
       const Unit un = P.units[u];
       const int k = un.k;
@@ -476,26 +542,35 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const bool row_ok = gi < n_k;
       const int ni25 = (int)(P.nq[pb + gi] >> 25);
       int row_count = 0;
+      const int64_t tpk = P.et.tp_off[k];
       for (int J = un.b0; J < un.b1; ++J) {
         const int col0 = J * kBN + ch * 64;           // first local column of this warp
+        const int64_t tile = tpk + tri_index(un.I, J, T);
         // Integer decision. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
         //   y >= r_in  => D2c <= t_in (certainly inside; a3, L.L >= 0)
         //   y <= r_out => D2c >  t_out (certainly outside; a3, L.L bounded)
         //   otherwise  => exact fp64 recheck in the element's order
         // r = floor(N_i/2^25) + per-tile constant (tile_thr_kernel, with the
         // margins that absorb every rounding).
-        const int64_t tile = P.et.tp_off[k] + tri_index(un.I, J, T);
-        const TileThr th = P.thr[tile];
-        const int r_in = th.k_in == kNever ? 0x7fffffff : ni25 + th.k_in;
-        const int r_out = th.k_out == kNever ? (int)0x80000000 : ni25 + th.k_out;
-        // floor(N_j / 2^25) of this warp's 64 columns: lane j holds columns j, 32 + j
-        const int cown0 = (int)(P.nq[pb + col0 + lane] >> 25);
-        const int cown1 = (int)(P.nq[pb + col0 + 32 + lane] >> 25);
+        EP_START();
+        mbar_wait(info_full + islot, ph_info[islot]);
+        ph_info[islot] ^= 1;
+        const int2 th = info[islot].th;
+        const int cown0 = info[islot].cq[ch * 64 + lane];
+        const int cown1 = info[islot].cq[ch * 64 + 32 + lane];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(info_empty + islot);
+        islot = (islot + 1) % kInfo;
+        // |y| <= kYMax for every pair, so clamping the bounds to +-(kYMax + 2)
+        // keeps every decision and rules out int32 overflow below
+        const int rin1 = th.x == kNever ? kYMax + 2 : max(-kYMax - 2, min(kYMax + 2, ni25 + th.x - 1));
+        const int ro1 = th.y == kNever ? -kYMax - 2 : max(-kYMax - 2, min(kYMax + 2, ni25 + th.y + 1));
         const uint32_t colmask0 = __ballot_sync(0xffffffffu, col0 + lane < n_k);
         const uint32_t colmask1 = __ballot_sync(0xffffffffu, col0 + 32 + lane < n_k);
         const uint32_t tq = tacc0 + ((uint32_t)(q * 32) << 16) + ch * 64;
         // --- phase 1: t1 = 256 a0 + a1 (exact int32), then release A0/A1
         mbar_wait(acc_full + 0, ph_acc[0]);
+        EP_MARK(0);
         tc_fence_after();
         int32_t t1[64];
 #pragma unroll
@@ -510,35 +585,49 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + 0);
-        // --- phase 2: decisions from A2
+        // --- phase 2: fold A2 into t1 (u = t1 + (a2 >> 8)), release A2 at once,
+        //     then decide from registers while the next tile's MMAs run
+        EP_MARK(2);
         mbar_wait(acc_full + 1, ph_acc[1]);
+        EP_MARK(1);
         tc_fence_after();
-        uint32_t in_w[2] = {0u, 0u}, amb_w[2] = {0u, 0u};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           int32_t a2[16];
           tmem_ld16(tq + 2 * kBN + h * 16, a2);
           tmem_ld_wait();
-          uint32_t iw = 0, ow = 0;
-          const int cown = (h < 2) ? cown0 : cown1;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int cj = __shfl_sync(0xffffffffu, cown, (h & 1) * 16 + j);
-            const int y = t1[h * 16 + j] + (a2[j] >> 8) - cj;
-            iw |= (y >= r_in ? 1u : 0u) << j;
-            ow |= (y <= r_out ? 1u : 0u) << j;
-          }
-          const int sh = (h & 1) * 16;
-          in_w[h >> 1] |= iw << sh;
-          amb_w[h >> 1] |= (~iw & ~ow & 0xffffu) << sh;
+          for (int j = 0; j < 16; ++j) t1[h * 16 + j] += a2[j] >> 8;
         }
-        in_w[0] &= row_ok ? colmask0 : 0u;
-        in_w[1] &= row_ok ? colmask1 : 0u;
-        amb_w[0] &= row_ok ? colmask0 : 0u;
-        amb_w[1] &= row_ok ? colmask1 : 0u;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + 1);
+
+        // Decision per pair from two sign bits (no predicates, no selects):
+        //   (r_in - 1) - y < 0  <=> certainly inside
+        //   y - (r_out + 1) < 0 <=> certainly outside
+        // each funnel-shifted into a row word (columns 31..0 -> bits 31..0);
+        // neither => undecided -> exact recheck queue.
+        uint32_t in_w[2], amb_w[2];
+        EP_MARK(3);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cown = h ? cown1 : cown0;
+          uint32_t wi_hi = 0, wi_lo = 0, wo_hi = 0, wo_lo = 0;
+#pragma unroll
+          for (int jj = 15; jj >= 0; --jj) {
+            const int y_hi = t1[h * 32 + 16 + jj] - __shfl_sync(0xffffffffu, cown, 16 + jj);
+            const int y_lo = t1[h * 32 + jj] - __shfl_sync(0xffffffffu, cown, jj);
+            wi_hi = __funnelshift_l((uint32_t)(rin1 - y_hi), wi_hi, 1);
+            wi_lo = __funnelshift_l((uint32_t)(rin1 - y_lo), wi_lo, 1);
+            wo_hi = __funnelshift_l((uint32_t)(y_hi - ro1), wo_hi, 1);
+            wo_lo = __funnelshift_l((uint32_t)(y_lo - ro1), wo_lo, 1);
+          }
+          const uint32_t valid = row_ok ? (h ? colmask1 : colmask0) : 0u;
+          const uint32_t iw = (wi_hi << 16) | wi_lo, ow = (wo_hi << 16) | wo_lo;
+          in_w[h] = iw & valid;
+          amb_w[h] = valid & ~iw & ~ow;
+        }
         ph_acc[0] ^= 1;
         ph_acc[1] ^= 1;
         // bitmap words (row, 2 x 32 columns) of tile (I, J)
@@ -561,7 +650,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
             if (my) atomicAdd(colcnt + cbank * kBN + ch * 64 + h * 32 + lane, my);
           }
         }
+        EP_MARK(4);
         epi_bar();
+        EP_MARK(5);
         if (J != un.I && q == 0) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -572,23 +663,44 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           }
         }
         cbank ^= 1;
-        // undecided pairs -> exact recheck queue
+        // undecided pairs -> exact recheck queue (one atomic per warp)
+        {
+          const int nb0 = __popc(amb_w[0]), nb = nb0 + __popc(amb_w[1]);
+          int incl = nb;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t band = amb_w[h];
-          if (band) {
-            unsigned long long i = atomicAdd(P.qcount, (unsigned long long)__popc(band));
-            while (band) {
-              const int j = __ffs(band) - 1;
-              band &= band - 1;
-              if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + h * 32 + j);
-              ++i;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int tot = __shfl_sync(0xffffffffu, incl, 31);
+          if (tot) {
+            unsigned long long base = 0;
+            if (lane == 31) base = atomicAdd(P.qcount, (unsigned long long)tot);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            unsigned long long i = base + (unsigned long long)(incl - nb);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t band = amb_w[h];
+              while (band) {
+                const int j = __ffs(band) - 1;
+                band &= band - 1;
+                if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + h * 32 + j);
+                ++i;
+              }
             }
           }
         }
+        EP_MARK(6);
       }
       if (row_count) atomicAdd(P.cnt + pb + gi, row_count);
     }
+#ifdef BM_TC_PROFILE
+    if (P.prof && ew == 0 && lane == 0) {
+      long long* pr = P.prof + 148 * 8 + blockIdx.x * 8;
+      for (int i = 0; i < 7; ++i) pr[i] = ep[i];
+      pr[7] = clock64() - ep_t0;
+    }
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -660,7 +772,8 @@ __global__ void elem_scale_kernel(int64_t d, ElemTables et, const int32_t* __res
 __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad,
                                 ElemTables et, int64_t P, const double* __restrict__ center,
                                 const double* __restrict__ scale, int8_t* __restrict__ planes,
-                                int64_t* __restrict__ nq, unsigned long long* __restrict__ tile_e) {
+                                int64_t* __restrict__ nq, int32_t* __restrict__ cq,
+                                unsigned long long* __restrict__ tile_e) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
@@ -702,6 +815,7 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
     }
     if (lane == 0) {
       nq[p] = nsum;
+      cq[p] = (int32_t)(nsum >> 25);
       if (valid) {
         // rigorous upper bound of |x - c - s q|: the fp64 evaluation of each
         // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
@@ -850,7 +964,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   double* center = s_cs.as<double>();
   double* scale = center + n_el * d;
   BM_TRY(scratch_alloc(s_pl, (size_t)3 * P * kpad, stream));
-  BM_TRY(scratch_alloc(s_nq, (size_t)P * 8, stream));
+  BM_TRY(scratch_alloc(s_nq, (size_t)P * 12, stream));
   BM_TRY(scratch_alloc(s_te, (size_t)n_tiles * 8, stream));
   BM_CHECK_CUDA(cudaMemsetAsync(s_te.ptr, 0, n_tiles * 8, stream));
   BM_TRY(scratch_alloc(s_units, n_units * sizeof(Unit), stream));
@@ -865,6 +979,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   BM_CHECK_LAUNCH();
   quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
       Xg, d, kpad, et, P, center, scale, s_pl.as<int8_t>(), s_nq.as<int64_t>(),
+      reinterpret_cast<int32_t*>(s_nq.as<int64_t>() + P),
       s_te.as<unsigned long long>());
   BM_CHECK_LAUNCH();
 
@@ -877,10 +992,12 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   unsigned long long qcap = std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 5000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
-  const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024;
+  const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;
   static bool attr = false;
   if (!attr) {
-    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel,
+    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel<2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
@@ -906,6 +1023,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     prm.units = s_units.as<Unit>();
     prm.n_units = n_units;
     prm.nq = s_nq.as<int64_t>();
+    prm.cq = reinterpret_cast<const int32_t*>(s_nq.as<int64_t>() + P);
     prm.tile_u = tile_u;
     prm.tbase = d_tbase;
     prm.a_in = a_in;
@@ -920,6 +1038,13 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     prm.P = P;
     prm.qcount = d_cnt;
     prm.qcap = qcap;
+    static const bool tc_prof = getenv("B200MAP_TC_PROFILE") != nullptr;
+    Scratch s_prof;
+    if (tc_prof) {
+      BM_TRY(scratch_alloc(s_prof, 148 * 8 * 8 * 2, stream));
+      BM_CHECK_CUDA(cudaMemsetAsync(s_prof.ptr, 0, 148 * 8 * 8 * 2, stream));
+      prm.prof = s_prof.as<long long>();
+    }
     prm.thr = s_tt.as<TileThr>();
     if (attempt == 0) {
       tile_thr_kernel<<<(unsigned)ceil_div(n_tp, 256), 256, 0, stream>>>(prm, n_tp,
@@ -927,10 +1052,32 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
       BM_CHECK_LAUNCH();
     }
     const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
-    tc_adjacency_kernel<<<grid, kThreads, smem, stream>>>(qmap, prm);
+    if (nkc == 1)
+      tc_adjacency_kernel<1><<<grid, kThreads, smem, stream>>>(qmap, prm);
+    else
+      tc_adjacency_kernel<2><<<grid, kThreads, smem, stream>>>(qmap, prm);
     BM_CHECK_LAUNCH();
     BM_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    if (tc_prof) {
+      std::vector<long long> pr(148 * 8 * 2);
+      BM_CHECK_CUDA(cudaMemcpy(pr.data(), s_prof.ptr, pr.size() * 8, cudaMemcpyDeviceToHost));
+      double t[5] = {0, 0, 0, 0, 0};
+      for (int b = 0; b < 148; ++b)
+        for (int i = 0; i < 5; ++i) t[i] += pr[b * 8 + i];
+      fprintf(stderr, "[tc-profile] MMA warp cycles/CTA: total %.3g  wait A %.1f%%  wait B %.1f%%  "
+              "wait acc01 %.1f%%  wait acc2 %.1f%%  (units %lld)\n", t[0] / 148,
+              100 * t[1] / t[0], 100 * t[2] / t[0], 100 * t[3] / t[0], 100 * t[4] / t[0],
+              (long long)n_units);
+      double e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int b = 0; b < 148; ++b)
+        for (int i = 0; i < 8; ++i) e[i] += pr[148 * 8 + b * 8 + i];
+      fprintf(stderr, "[tc-profile] epilogue warp: wait acc01 %.1f%%  E1 %.1f%%  wait acc2 %.1f%%  "
+              "fold %.1f%%  decide+pack %.1f%%  epi_bar %.1f%%  flush+queue %.1f%%  rest %.1f%%\n",
+              100 * e[0] / e[7], 100 * e[2] / e[7], 100 * e[1] / e[7], 100 * e[3] / e[7],
+              100 * e[4] / e[7], 100 * e[5] / e[7], 100 * e[6] / e[7],
+              100 * (e[7] - e[0] - e[1] - e[2] - e[3] - e[4] - e[5] - e[6]) / e[7]);
+    }
     if (h_cnt[0] <= qcap) break;
     qcap = h_cnt[0] + 1024;
     if (attempt == 2) {

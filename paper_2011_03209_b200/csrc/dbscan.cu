@@ -259,27 +259,29 @@ adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, 
 // counts from the bitmap: rows of every tile, columns of off-diagonal tiles
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128)
-count_kernel(const uint32_t* __restrict__ adj, ElemTables et, int64_t n_tp,
-             int32_t* __restrict__ cnt) {
+count_kernel(const uint32_t* __restrict__ adj, ElemTables et, const TileUnit* __restrict__ units,
+             int64_t n_units, int32_t* __restrict__ cnt) {
   __shared__ uint32_t bits[kTileWords];
-  for (int64_t g = blockIdx.x; g < n_tp; g += gridDim.x) {
-    int k, I, J;
-    decode_tile(et, g, k, I, J);
-    const int64_t pb = et.pbase[k];
-    __syncthreads();
-    const uint4* src = reinterpret_cast<const uint4*>(adj + g * kTileWords);
-    uint4 w = src[threadIdx.x];
-    reinterpret_cast<uint4*>(bits)[threadIdx.x] = w;
-    int rc = __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
-    if (rc) atomicAdd(cnt + pb + I * kTile + threadIdx.x, rc);
-    if (I != J) {
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const TileUnit un = units[u];
+    const int64_t pb = et.pbase[un.k], tpk = et.tp_off[un.k], T = et.ntiles[un.k];
+    int rc = 0;
+    for (int J = un.J0; J < un.J1; ++J) {
+      const int64_t g = tpk + tri_index(un.I, J, T);
       __syncthreads();
-      const int c = threadIdx.x, wd = c >> 5, sh = c & 31;
-      int cc = 0;
+      const uint4 w = reinterpret_cast<const uint4*>(adj + g * kTileWords)[threadIdx.x];
+      reinterpret_cast<uint4*>(bits)[threadIdx.x] = w;
+      rc += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+      if (J != un.I) {
+        __syncthreads();
+        const int c = threadIdx.x, wd = c >> 5, sh = c & 31;
+        int cc = 0;
 #pragma unroll 8
-      for (int r = 0; r < kTile; ++r) cc += (bits[r * 4 + wd] >> sh) & 1u;
-      if (cc) atomicAdd(cnt + pb + J * kTile + c, cc);
+        for (int r = 0; r < kTile; ++r) cc += (bits[r * 4 + wd] >> sh) & 1u;
+        if (cc) atomicAdd(cnt + pb + J * kTile + c, cc);
+      }
     }
+    if (rc) atomicAdd(cnt + pb + un.I * kTile + threadIdx.x, rc);
   }
 }
 
@@ -319,7 +321,8 @@ __device__ __forceinline__ bool lunion(int* lp, int a, int b) {
 
 template <bool DIAG>
 __global__ void __launch_bounds__(128)
-components_kernel(const uint32_t* __restrict__ adj, ElemTables et, int64_t n_tp,
+components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
+                  const TileUnit* __restrict__ units, int64_t n_units,
                   const uint8_t* __restrict__ core, int32_t* __restrict__ par,
                   int32_t* __restrict__ bmin) {
   __shared__ uint32_t bits[kTileWords];
@@ -328,71 +331,85 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et, int64_t n_tp,
   __shared__ uint32_t coreJ[4], coreI[4];
   __shared__ int any_merge;
   const int t = threadIdx.x;
-  for (int64_t g = blockIdx.x; g < n_tp; g += gridDim.x) {
-    int k, I, J;
-    decode_tile(et, g, k, I, J);
-    if (DIAG != (I == J)) continue;  // uniform
-    const int64_t pb = et.pbase[k];
-    const int pI = (int)(pb + I * kTile), pJ = (int)(pb + J * kTile);
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const TileUnit un = units[u];
+    const int k = un.k, I = un.I;
+    const int64_t pb = et.pbase[k], tpk = et.tp_off[k], T = et.ntiles[k];
+    const int nk = et.nrows[k];
+    const int pI = (int)(pb + I * kTile);
+    // row side once per unit (stale roots later only cost redundant unions)
+    const bool ci = core[pI + t];
+    int gr = ci ? uf_find(par, pI + t) : -1;
     __syncthreads();
-    reinterpret_cast<uint4*>(bits)[t] = reinterpret_cast<const uint4*>(adj + g * kTileWords)[t];
-    const bool ci = core[pI + t], cj = core[pJ + t];
-    unsigned bi = __ballot_sync(0xffffffffu, ci), bj = __ballot_sync(0xffffffffu, cj);
-    if ((t & 31) == 0) { coreI[t >> 5] = bi; coreJ[t >> 5] = bj; }
-    groot[t] = ci ? uf_find(par, pI + t) : -1;
-    groot[kTile + t] = (!DIAG && cj) ? uf_find(par, pJ + t) : -1;
-    lp[t] = t;
-    lp[kTile + t] = kTile + t;
-    if (t == 0) any_merge = 0;
-    __syncthreads();
-    // --- core-core edges between nodes with different global roots
-    const int r = t;
-    if (ci) {
-      const int gr = groot[r];
+    {
+      const unsigned bi = __ballot_sync(0xffffffffu, ci);
+      if ((t & 31) == 0) coreI[t >> 5] = bi;
+    }
+    for (int J = un.J0; J < un.J1; ++J) {
+      const int64_t g = tpk + tri_index(I, J, T);
+      const int pJ = (int)(pb + J * kTile);
+      __syncthreads();
+      reinterpret_cast<uint4*>(bits)[t] = reinterpret_cast<const uint4*>(adj + g * kTileWords)[t];
+      const bool cj = DIAG ? ci : (bool)core[pJ + t];
+      if (!DIAG) {
+        const unsigned bj = __ballot_sync(0xffffffffu, cj);
+        if ((t & 31) == 0) coreJ[t >> 5] = bj;
+      }
+      groot[t] = gr;
+      groot[kTile + t] = (!DIAG && cj) ? uf_find(par, pJ + t) : -1;
+      lp[t] = t;
+      lp[kTile + t] = kTile + t;
+      if (t == 0) any_merge = 0;
+      __syncthreads();
+      // --- core-core edges between nodes with different global roots
+      const int r = t;
+      if (ci) {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
-        while (m) {
-          const int c = w * 32 + __ffs(m) - 1;
-          m &= m - 1;
-          const int node = DIAG ? c : kTile + c;
-          if (groot[node] != gr) {
-            if (lunion(lp, r, node)) any_merge = 1;
+        for (int w = 0; w < 4; ++w) {
+          uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
+          while (m) {
+            const int c = w * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            const int node = DIAG ? c : kTile + c;
+            if (groot[node] != gr) {
+              if (lunion(lp, r, node)) any_merge = 1;
+            }
           }
         }
       }
-    }
-    // --- border: non-core row r -> smallest core column
-    if (!ci && r < et.nrows[k] - I * kTile) {
+      // --- border: non-core row r -> smallest core column
+      if (!ci && r < nk - I * kTile) {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
-        if (m) {
-          const int c = w * 32 + __ffs(m) - 1;
-          const int cand = (DIAG ? pI : pJ) + c;
-          if (cand < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, cand);
-          break;
+        for (int w = 0; w < 4; ++w) {
+          uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
+          if (m) {
+            const int c = w * 32 + __ffs(m) - 1;
+            const int cand = (DIAG ? pI : pJ) + c;
+            if (cand < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, cand);
+            break;
+          }
         }
       }
-    }
-    // --- border: non-core column c -> smallest core row (off-diagonal only)
-    if (!DIAG && !cj && t < et.nrows[k] - J * kTile) {
-      const int c = t, wd = c >> 5, sh = c & 31;
-      for (int rr = 0; rr < kTile; ++rr) {
-        if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u)) {
-          const int cand = pI + rr;
-          if (cand < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, cand);
-          break;
+      // --- border: non-core column c -> smallest core row (off-diagonal only)
+      if (!DIAG && !cj && t < nk - J * kTile) {
+        const int c = t, wd = c >> 5, sh = c & 31;
+        for (int rr = 0; rr < kTile; ++rr) {
+          if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u)) {
+            const int cand = pI + rr;
+            if (cand < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, cand);
+            break;
+          }
         }
       }
-    }
-    __syncthreads();
-    // --- propagate local merges to the global forest
-    if (any_merge) {
-      for (int x = t; x < 2 * kTile; x += blockDim.x) {
-        if (groot[x] < 0) continue;
-        const int lr = lfind(lp, x);
-        if (lr != x && groot[lr] != groot[x]) uf_union(par, groot[x], groot[lr]);
+      __syncthreads();
+      // --- propagate local merges to the global forest
+      if (any_merge) {
+        for (int x = t; x < 2 * kTile; x += blockDim.x) {
+          if (groot[x] < 0) continue;
+          const int lr = lfind(lp, x);
+          if (lr != x && groot[lr] != groot[x]) uf_union(par, groot[x], groot[lr]);
+        }
+        if (ci) gr = uf_find(par, gr);  // refresh the row roots after merges
       }
     }
   }
@@ -662,7 +679,25 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     uint8_t* core = (uint8_t*)(hscan + P + 1);
     BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
-    const unsigned tgrid = grid_for(n_tp, 1, 32);
+    // row-tile units: diagonal tiles, and off-diagonal ranges of <= 32 tiles
+    std::vector<TileUnit> hunits;
+    int64_t n_diag = 0;
+    for (int64_t i = 0; i < nb_el; ++i) {
+      for (int32_t I = 0; I < ntiles[i]; ++I) hunits.push_back({(int32_t)i, I, I, I + 1});
+    }
+    n_diag = (int64_t)hunits.size();
+    for (int64_t i = 0; i < nb_el; ++i)
+      for (int32_t I = 0; I < ntiles[i]; ++I)
+        for (int32_t J0 = I + 1; J0 < ntiles[i]; J0 += 32)
+          hunits.push_back({(int32_t)i, I, J0, std::min<int32_t>(J0 + 32, ntiles[i])});
+    const int64_t n_off = (int64_t)hunits.size() - n_diag;
+    Scratch s_units;
+    BM_TRY(scratch_alloc(s_units, std::max<size_t>(1, hunits.size()) * sizeof(TileUnit), stream));
+    if (!hunits.empty())
+      BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, hunits.data(), hunits.size() * sizeof(TileUnit),
+                                    cudaMemcpyHostToDevice, stream));
+    const TileUnit* d_diag = s_units.as<TileUnit>();
+    const TileUnit* d_off = d_diag + n_diag;
 
     // ---- adjacency bitmap
     Scratch adj;
@@ -685,18 +720,20 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
 
     // ---- counts, core, union-find, border
     if (!use_tc) {
-      count_kernel<<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, cnt);
+      count_kernel<<<grid_for(n_diag + n_off, 1, 32), 128, 0, stream>>>(adj.as<uint32_t>(), et,
+                                                                       d_diag, n_diag + n_off, cnt);
       BM_CHECK_LAUNCH();
     }
     core_init_kernel<<<grid_for(P, 256), 256, 0, stream>>>(cnt, et, P, min_pts, core, par, bmin);
     BM_CHECK_LAUNCH();
-    components_kernel<true><<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, core, par,
-                                                       bmin);
+    components_kernel<true><<<grid_for(n_diag, 1, 32), 128, 0, stream>>>(adj.as<uint32_t>(), et,
+                                                                         d_diag, n_diag, core, par, bmin);
     BM_CHECK_LAUNCH();
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par, core, P);
     BM_CHECK_LAUNCH();
-    components_kernel<false><<<tgrid, 128, 0, stream>>>(adj.as<uint32_t>(), et, n_tp, core, par,
-                                                        bmin);
+    if (n_off > 0)
+      components_kernel<false><<<grid_for(n_off, 1, 32), 128, 0, stream>>>(
+          adj.as<uint32_t>(), et, d_off, n_off, core, par, bmin);
     BM_CHECK_LAUNCH();
     label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par, bmin, lab, cmin);
     BM_CHECK_LAUNCH();

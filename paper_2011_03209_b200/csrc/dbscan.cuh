@@ -29,6 +29,11 @@ struct ElemTables {
   int64_t n_el;
 };
 
+// row-tile work unit: element k, row tile I, column tiles [J0, J1)
+struct TileUnit {
+  int32_t k, I, J0, J1;
+};
+
 __device__ __forceinline__ int64_t tri_index(int64_t I, int64_t J, int64_t T) {
   return I * T - I * (I - 1) / 2 + (J - I);
 }

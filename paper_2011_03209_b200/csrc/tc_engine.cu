@@ -8,7 +8,7 @@
 // MMA accumulation has no documented rounding model; integer MMA
 // (kind::i8, s32 accumulate) is exact. Each element is centred (c_k) and
 // quantised to 24-bit fixed point q = rint((x - c_k) / s_k), split into
-// three 8-bit limbs q = H*2^16 + M*2^8 + L (H signed, M/L unsigned). The
+// three limbs q = H*2^14 + M*2^7 + L (H signed 8-bit, M/L in [0,127]). The
 // dot product q_i.q_j is the exact sum of 9 limb products; 8 run on the
 // tensor cores (the L.L term, 0 <= LL <= 255^2 d, is bounded instead),
 // accumulated per shift class in 4 TMEM accumulators:
@@ -57,7 +57,9 @@ constexpr int kInfo = 3;        // per-tile info ring depth (smem)
 constexpr int kEpiWarps = 8;    // epilogue warps 4..11
 constexpr int kLoadWarps = 4;   // A-loader warps 12..15
 constexpr int kThreads = 128 + 32 * (kEpiWarps + kLoadWarps);
-constexpr int kQBits = 22;      // |q| <= 2^22 - 1 (H in [-64, 63]: every y below fits in int32)
+constexpr int kLimb = 7;        // bits of the M and L limbs
+constexpr int kQBits = 2 * kLimb + 7;   // |q| <= 2^21 - 1: H = q >> 14 is a signed byte
+constexpr int kYShift = 3 * kLimb + 1;  // y is in units of 2^22 of D2
 
 struct Unit {
   int32_t k, I, b0, b1;
@@ -183,7 +185,7 @@ constexpr int32_t kNever = 0x7fffffff;
 #define EP_START() ((void)0)
 #define EP_MARK(i) ((void)0)
 #endif
-constexpr int kYMax = 500000000;  // bound on |y| (kQBits = 22, Kpad <= 256)
+constexpr int kYMax = 850000000;  // bound on |y| (kLimb = 7, Kpad <= 256): see tc_engine header
 
 struct TcParams {
   ElemTables et;
@@ -191,7 +193,7 @@ struct TcParams {
   const Unit* units;
   int64_t n_units;
   const int64_t* nq;      // per padded row: sum q^2
-  const int32_t* cq;      // per padded row: floor(sum q^2 / 2^25)
+  const int32_t* cq;      // per padded row: floor(sum q^2 / 2^kYShift)
   const double* tile_u;   // per 128-row tile: max quantisation error / s_k (quantised units)
   const int32_t* tbase;   // per element: first global 128-row tile index
   const double* a_in;     // per element: eps / (1 + gamma) / s_k
@@ -228,9 +230,10 @@ __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI,
 }
 
 // Per bitmap tile pair: exact thresholds t_in/t_out on D2c and the integer
-// offsets of the fast path (see the epilogue): with ni25 = floor(N_i/2^25),
-//   r_in  = ni25 + ceil(-t_in/2^25) + 3   >= (N_i - t_in)/2^25 + 2
-//   r_out = ni25 + floor(-(t_out + a3max)/2^25) - 2 <= (N_i - t_out - a3max)/2^25 - 1
+// offsets of the fast path (see the epilogue): with U = 2^kYShift and
+// niU = floor(N_i/U),
+//   r_in  = niU + ceil(-t_in/U) + 3   >= (N_i - t_in)/U + 2
+//   r_out = niU + floor(-(t_out + a3max)/U) - 2 <= (N_i - t_out - a3max)/U - 1
 __global__ void tile_thr_kernel(TcParams P, int64_t n_tp, TileThr* __restrict__ out) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_tp) return;
@@ -241,7 +244,7 @@ __global__ void tile_thr_kernel(TcParams P, int64_t n_tp, TileThr* __restrict__ 
   TileThr th;
   th.t_in = t_in;
   th.t_out = t_out;
-  const double sc = 1.0 / 33554432.0;
+  const double sc = 1.0 / (double)(1ll << kYShift);
   th.k_in = t_in > -1e18 ? (int32_t)fmin(fmax(ceil(-t_in * sc) + 3.0, -1073741824.0), 1073741824.0)
                          : kNever;
   // clamping k_in down is conservative (fewer certain-inside pairs); k_out
@@ -316,7 +319,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
   int32_t* colcnt = (int32_t*)(tmem_slot + 4);            // [2][kBN]
-  // per-tile info ring, filled ahead by the producer: floor(N_j/2^25) of the
+  // per-tile info ring, filled ahead by the producer: floor(N_j/U) of the
   // tile's 128 columns (bulk TMA) + the tile's integer threshold offsets
   struct TileInfo {
     int32_t cq[kBN];
@@ -540,17 +543,17 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       const int64_t T = P.et.ntiles[k];
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
-      const int ni25 = (int)(P.nq[pb + gi] >> 25);
+      const int niU = (int)(P.nq[pb + gi] >> kYShift);
       int row_count = 0;
       const int64_t tpk = P.et.tp_off[k];
       for (int J = un.b0; J < un.b1; ++J) {
         const int col0 = J * kBN + ch * 64;           // first local column of this warp
         const int64_t tile = tpk + tri_index(un.I, J, T);
-        // Integer decision. With y = 256 a0 + a1 + (a2 >> 8) - floor(N_j/2^25):
+        // Integer decision. With y = 2^7 a0 + a1 + (a2 >> 7) - floor(N_j/U):
         //   y >= r_in  => D2c <= t_in (certainly inside; a3, L.L >= 0)
         //   y <= r_out => D2c >  t_out (certainly outside; a3, L.L bounded)
         //   otherwise  => exact fp64 recheck in the element's order
-        // r = floor(N_i/2^25) + per-tile constant (tile_thr_kernel, with the
+        // r = floor(N_i/U) + per-tile constant (tile_thr_kernel, with the
         // margins that absorb every rounding).
         EP_START();
         mbar_wait(info_full + islot, ph_info[islot]);
@@ -563,8 +566,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         islot = (islot + 1) % kInfo;
         // |y| <= kYMax for every pair, so clamping the bounds to +-(kYMax + 2)
         // keeps every decision and rules out int32 overflow below
-        const int rin1 = th.x == kNever ? kYMax + 2 : max(-kYMax - 2, min(kYMax + 2, ni25 + th.x - 1));
-        const int ro1 = th.y == kNever ? -kYMax - 2 : max(-kYMax - 2, min(kYMax + 2, ni25 + th.y + 1));
+        const int rin1 = th.x == kNever ? kYMax + 2 : max(-kYMax - 2, min(kYMax + 2, niU + th.x - 1));
+        const int ro1 = th.y == kNever ? -kYMax - 2 : max(-kYMax - 2, min(kYMax + 2, niU + th.y + 1));
         const uint32_t colmask0 = __ballot_sync(0xffffffffu, col0 + lane < n_k);
         const uint32_t colmask1 = __ballot_sync(0xffffffffu, col0 + 32 + lane < n_k);
         const uint32_t tq = tacc0 + ((uint32_t)(q * 32) << 16) + ch * 64;
@@ -580,7 +583,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           tmem_ld16(tq + 1 * kBN + h * 16, x1);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) t1[h * 16 + j] = x0[j] * 256 + x1[j];
+          for (int j = 0; j < 16; ++j) t1[h * 16 + j] = x0[j] * (1 << kLimb) + x1[j];
         }
         tc_fence_before();
         __syncwarp();
@@ -597,7 +600,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           tmem_ld16(tq + 2 * kBN + h * 16, a2);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) t1[h * 16 + j] += a2[j] >> 8;
+          for (int j = 0; j < 16; ++j) t1[h * 16 + j] += a2[j] >> kLimb;
         }
         tc_fence_before();
         __syncwarp();
@@ -804,9 +807,9 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
         ysum += y * y;
       }
       nsum += (long long)q * q;
-      hp[c] = (int8_t)(q >> 16);
-      mp[c] = (uint8_t)((q >> 8) & 255);
-      lp[c] = (uint8_t)(q & 255);
+      hp[c] = (int8_t)(q >> (2 * kLimb));
+      mp[c] = (uint8_t)((q >> kLimb) & ((1 << kLimb) - 1));
+      lp[c] = (uint8_t)(q & ((1 << kLimb) - 1));
     }
     for (int o = 16; o; o >>= 1) {
       nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
@@ -815,7 +818,7 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
     }
     if (lane == 0) {
       nq[p] = nsum;
-      cq[p] = (int32_t)(nsum >> 25);
+      cq[p] = (int32_t)(nsum >> kYShift);
       if (valid) {
         // rigorous upper bound of |x - c - s q|: the fp64 evaluation of each
         // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
@@ -846,13 +849,30 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
   }
 }
 
-// exact recheck of the queued pairs in the element's fp64 order
+// exact recheck of the queued pairs in the element's fp64 order; one warp per
+// pair: coalesced row loads and squares in parallel, then the reference's
+// exact summation order over the squares (sequential: a left-to-right
+// shuffle chain; pairwise: exact_dist2 on lane 0 from the cached rows)
+__device__ __forceinline__ void set_inside(const ElemTables& et, int k, int2 pr,
+                                           uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
+                                           unsigned long long* __restrict__ n_inside) {
+  const int li = pr.x - et.pbase[k], lj = pr.y - et.pbase[k];
+  const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
+  const int64_t tile = et.tp_off[k] + tri_index(I, J, et.ntiles[k]);
+  atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
+  atomicAdd(cnt + pr.x, 1);
+  if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
+  atomicAdd(n_inside, 1ull);
+}
+
 __global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
                                const int2* __restrict__ queue, int64_t nq, double eps,
                                uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
                                unsigned long long* __restrict__ n_inside) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < nq;
+       i += (int64_t)gridDim.x * wpb) {
     const int2 pr = queue[i];
     int64_t a = 0, bb = et.n_el;
     while (bb - a > 1) {
@@ -860,17 +880,27 @@ __global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTab
       if (et.pbase[mid] <= pr.x) a = mid; else bb = mid;
     }
     const int k = (int)a;
-    const double s2 = exact_dist2(Xg + (int64_t)pr.x * d, Xg + (int64_t)pr.y * d, d,
-                                  et.order[k], c_prog_tc);
-    if (__dsqrt_rn(s2) <= eps) {
-      const int li = pr.x - et.pbase[k], lj = pr.y - et.pbase[k];
-      const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
-      const int64_t tile = et.tp_off[k] + tri_index(I, J, et.ntiles[k]);
-      atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
-      atomicAdd(cnt + pr.x, 1);
-      if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
-      atomicAdd(n_inside, 1ull);
+    const double* xa = Xg + (int64_t)pr.x * d;
+    const double* xb = Xg + (int64_t)pr.y * d;
+    double s2;
+    if (et.order[k] == BM_ORDER_SEQUENTIAL) {
+      double s = 0.0;  // s = 0; s += (x_c - y_c)^2 for c = 0..d-1, exactly as cdist
+      for (int64_t c0 = 0; c0 < d; c0 += 32) {
+        const int64_t c = c0 + lane;
+        double sq = 0.0;
+        if (c < d) {
+          const double df = __dsub_rn(xa[c], xb[c]);
+          sq = __dmul_rn(df, df);
+        }
+        const int n = (d - c0) < 32 ? (int)(d - c0) : 32;
+        for (int j = 0; j < n; ++j) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, j));
+      }
+      s2 = s;
+    } else {
+      s2 = lane == 0 ? exact_dist2(xa, xb, d, BM_ORDER_PAIRWISE, c_prog_tc) : 0.0;
+      s2 = __shfl_sync(0xffffffffu, s2, 0);
     }
+    if (lane == 0 && __dsqrt_rn(s2) <= eps) set_inside(et, k, pr, adj, cnt, n_inside);
   }
 }
 
@@ -1028,8 +1058,9 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     prm.tbase = d_tbase;
     prm.a_in = a_in;
     prm.a_out = a_out;
-    prm.ll2 = 2.0 * 255.0 * 255.0 * (double)kpad;
-    prm.a3max = 512.0 * 2.0 * 255.0 * 255.0 * (double)kpad;
+    const double lmax = (double)((1 << kLimb) - 1);
+    prm.ll2 = 2.0 * lmax * lmax * (double)kpad;                           // 2 L.L
+    prm.a3max = (double)(2 << kLimb) * 2.0 * lmax * lmax * (double)kpad;  // 2^(b+1) A3
     prm.nkc = nkc;
     prm.adj = adj;
     prm.cnt = cnt;
@@ -1087,7 +1118,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   }
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
-    recheck_kernel<<<grid_cap(nrec, 128, 16), 128, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
+    recheck_kernel<<<grid_cap(nrec * 32, 256, 16), 256, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
                                                                 eps, adj, cnt, d_cnt + 1);
     BM_CHECK_LAUNCH();
   }

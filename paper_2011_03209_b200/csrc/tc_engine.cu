@@ -849,10 +849,6 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
   }
 }
 
-// exact recheck of the queued pairs in the element's fp64 order; one warp per
-// pair: coalesced row loads and squares in parallel, then the reference's
-// exact summation order over the squares (sequential: a left-to-right
-// shuffle chain; pairwise: exact_dist2 on lane 0 from the cached rows)
 __device__ __forceinline__ void set_inside(const ElemTables& et, int k, int2 pr,
                                            uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
                                            unsigned long long* __restrict__ n_inside) {
@@ -865,42 +861,111 @@ __device__ __forceinline__ void set_inside(const ElemTables& et, int k, int2 pr,
   atomicAdd(n_inside, 1ull);
 }
 
-__global__ void recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
-                               const int2* __restrict__ queue, int64_t nq, double eps,
-                               uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
-                               unsigned long long* __restrict__ n_inside) {
+// exact recheck of the queued pairs in the element's fp64 order. One lane per
+// pair, 32 pairs per warp: the warp stages 32-dim chunks of the squared
+// differences of its 32 pairs in shared memory with coalesced row loads, then
+// each lane folds its own pair's squares in dim order. Both reference orders
+// consume the dims left to right: sequential is s += v; pairwise (numpy's
+// add.reduce, PwProgram) keeps 8 strided accumulators per leaf. Leaf starts
+// are multiples of 8 (every left half has a length divisible by 8), so each
+// 8-dim group lies inside one leaf and maps accumulator j to dim 8g+j
+// statically; the leaf walk is uniform across lanes.
+constexpr int kRcWarps = 4;
+
+__global__ void __launch_bounds__(kRcWarps * 32)
+    recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+                   const int2* __restrict__ queue, int64_t nq, double eps,
+                   uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
+                   unsigned long long* __restrict__ n_inside) {
+  __shared__ double sq_all[kRcWarps][32][33];
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < nq;
-       i += (int64_t)gridDim.x * wpb) {
-    const int2 pr = queue[i];
-    int64_t a = 0, bb = et.n_el;
-    while (bb - a > 1) {
-      int64_t mid = (a + bb) >> 1;
-      if (et.pbase[mid] <= pr.x) a = mid; else bb = mid;
-    }
-    const int k = (int)a;
-    const double* xa = Xg + (int64_t)pr.x * d;
-    const double* xb = Xg + (int64_t)pr.y * d;
-    double s2;
-    if (et.order[k] == BM_ORDER_SEQUENTIAL) {
-      double s = 0.0;  // s = 0; s += (x_c - y_c)^2 for c = 0..d-1, exactly as cdist
-      for (int64_t c0 = 0; c0 < d; c0 += 32) {
-        const int64_t c = c0 + lane;
-        double sq = 0.0;
-        if (c < d) {
-          const double df = __dsub_rn(xa[c], xb[c]);
-          sq = __dmul_rn(df, df);
-        }
-        const int n = (d - c0) < 32 ? (int)(d - c0) : 32;
-        for (int j = 0; j < n; ++j) s = __dadd_rn(s, __shfl_sync(0xffffffffu, sq, j));
+  double(*S)[33] = sq_all[threadIdx.x >> 5];
+  const int64_t stride = (int64_t)gridDim.x * kRcWarps * 32;
+  for (int64_t base = ((int64_t)blockIdx.x * kRcWarps + (threadIdx.x >> 5)) * 32; base < nq;
+       base += stride) {
+    const int64_t i = base + lane;
+    const bool have = i < nq;
+    const int2 pr = have ? queue[i] : make_int2(0, 0);
+    int k = 0;
+    if (have) {
+      int64_t a = 0, bb = et.n_el;
+      while (bb - a > 1) {
+        const int64_t mid = (a + bb) >> 1;
+        if (et.pbase[mid] <= pr.x) a = mid; else bb = mid;
       }
-      s2 = s;
-    } else {
-      s2 = lane == 0 ? exact_dist2(xa, xb, d, BM_ORDER_PAIRWISE, c_prog_tc) : 0.0;
-      s2 = __shfl_sync(0xffffffffu, s2, 0);
+      k = (int)a;
     }
-    if (lane == 0 && __dsqrt_rn(s2) <= eps) set_inside(et, k, pr, adj, cnt, n_inside);
+    const int np = (nq - base) < 32 ? (int)(nq - base) : 32;
+    double s_seq = 0.0, res = 0.0;
+    double r[8];
+    PwStack st;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxStack; ++j) st.s[j] = 0.0;
+    int li = 0;
+    for (int64_t c0 = 0; c0 < d; c0 += 32) {
+      const bool cv = c0 + lane < d;
+#pragma unroll 4
+      for (int p = 0; p < np; ++p) {
+        const int64_t ra = __shfl_sync(0xffffffffu, pr.x, p);
+        const int64_t rb = __shfl_sync(0xffffffffu, pr.y, p);
+        double v = 0.0;
+        if (cv) {
+          const double df = __dsub_rn(Xg[ra * d + c0 + lane], Xg[rb * d + c0 + lane]);
+          v = __dmul_rn(df, df);
+        }
+        S[p][lane] = v;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int64_t gb = c0 + 8 * g;
+        if (gb >= d) break;
+        const int nv = (d - gb) < 8 ? (int)(d - gb) : 8;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = S[lane][8 * g + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < nv) s_seq = __dadd_rn(s_seq, v[j]);
+        const PwLeaf L = c_prog_tc.leaf[li];
+        const int pos = (int)(gb - L.start);
+        const int body = L.len - (L.len & 7);
+        bool finish = false;
+        if (L.len < 8) {
+          double rr = -0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < L.len) rr = __dadd_rn(rr, v[j]);
+          res = rr;
+          finish = true;
+        } else if (pos < body) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) r[j] = pos == 0 ? v[j] : __dadd_rn(r[j], v[j]);
+          if (pos + 8 == body) {
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            finish = body == L.len;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < L.len - body) res = __dadd_rn(res, v[j]);
+          finish = true;
+        }
+        if (finish) {
+          st.push(res);
+          for (int q = 0; q < L.pops; ++q) st.reduce();
+          ++li;
+        }
+      }
+      __syncwarp();
+    }
+    if (have) {
+      const double s2 = et.order[k] == BM_ORDER_SEQUENTIAL ? s_seq : __dadd_rn(0.0, st.s[0]);
+      if (__dsqrt_rn(s2) <= eps) set_inside(et, k, pr, adj, cnt, n_inside);
+    }
   }
 }
 
@@ -1118,7 +1183,7 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   }
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
-    recheck_kernel<<<grid_cap(nrec * 32, 256, 16), 256, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
+    recheck_kernel<<<grid_cap(nrec, kRcWarps * 32, 8), kRcWarps * 32, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
                                                                 eps, adj, cnt, d_cnt + 1);
     BM_CHECK_LAUNCH();
   }

@@ -118,6 +118,38 @@ int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
 int bm_pairwise_distances(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
                           int64_t n_rows, int order, double* d_out, void* stream);
 
+/* ---- row-block protocol: one huge element over several ranks -------------
+ * SURVEY §8e "huge single element" (cfg5). The element's eps-graph is a
+ * triangle of T x T bit tiles (128 rows each); ranks take disjoint windows of
+ * tile rows [I0, I1) (balanced by tile area) and run these per-rank steps; the
+ * host does the collectives (torch.distributed / NCCL) in between:
+ *   bm_big_open            gather + quantise the element's rows (once per rank)
+ *   bm_big_counts          bits of a window; eps-neighbour counts of every row
+ *                          they touch ADDED into d_cnt        -> all_reduce(sum)
+ *   bm_big_init            core = cnt >= min_pts; par[p] = p; bmin[p] = INT_MAX
+ *   bm_big_components      union-find over the window's core-core bits (in
+ *                          d_par) and border minima (in d_bmin) -> par gathered
+ *                          to rank 0 + bm_merge_forest; all_reduce(min) of bmin
+ *   bm_big_labels          canonical labels of the element's entries (rank 0)
+ * Arrays d_cnt/d_par/d_bmin hold P = 128 * T padded rows (int32); the caller
+ * zeroes d_cnt before the first bm_big_counts. All calls on a handle run on the
+ * stream given to bm_big_open. The same element processed by one rank with one
+ * window is exactly bm_cluster_elements (which uses this path itself, on one
+ * device, for an element whose bitmap exceeds the device budget).
+ * Reference: clustering.py:151-198 (the dbscan of one element). */
+int bm_big_open(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
+                int64_t n_rows, double eps, int32_t min_pts, int order, int engine,
+                void* stream, void** handle, int64_t* h_tiles);
+int bm_big_counts(void* handle, int32_t I0, int32_t I1, int32_t* d_cnt);
+int bm_big_init(void* handle, const int32_t* d_cnt, int32_t* d_par, int32_t* d_bmin);
+int bm_big_components(void* handle, int32_t I0, int32_t I1, int32_t* d_par, int32_t* d_bmin);
+int bm_big_labels(void* handle, int32_t* d_par, const int32_t* d_bmin, int32_t* d_labels,
+                  int32_t* h_n_clusters);
+int bm_big_stats(void* handle, int64_t* h_stats);
+int bm_big_close(void* handle);
+/* d_par := union of the forests d_par and d_other (n entries each). */
+int bm_merge_forest(int32_t* d_par, const int32_t* d_other, int64_t n, void* stream);
+
 /* ---- nodes (nerve.py:84-101): stable grouping of entries into node rows ----
  * Given per-entry labels (above) and the per-element cluster counts, writes
  * the rows of node v (dense ids in (element, cluster) order) into

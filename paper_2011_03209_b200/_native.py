@@ -52,6 +52,15 @@ _SIGNATURES = {
     "bm_cluster_elements": (ctypes.c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_i64, ctypes.c_double,
                                            _c_i32, _vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "bm_pairwise_distances": (ctypes.c_int, [_vp, _c_i64, _c_i64, _vp, _c_i64, ctypes.c_int, _vp, _vp]),
+    "bm_big_open": (ctypes.c_int, [_vp, _c_i64, _c_i64, _vp, _c_i64, ctypes.c_double, _c_i32,
+                                   ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "bm_big_counts": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp]),
+    "bm_big_init": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "bm_big_components": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _vp]),
+    "bm_big_labels": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "bm_big_stats": (ctypes.c_int, [_vp, _vp]),
+    "bm_big_close": (ctypes.c_int, [_vp]),
+    "bm_merge_forest": (ctypes.c_int, [_vp, _vp, _c_i64, _vp]),
     "bm_group_nodes": (ctypes.c_int, [_vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bm_nerve_edges": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
     "bm_node_stats": (ctypes.c_int, [_vp, _c_i64, _vp, ctypes.c_int, _vp, _vp, _c_i64, _vp, _vp, _vp]),

@@ -65,8 +65,11 @@ struct Scratch {
   Scratch() = default;
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
-  ~Scratch() {
+  ~Scratch() { release(); }
+  void release() {
     if (ptr) cudaFreeAsync(ptr, stream);
+    ptr = nullptr;
+    bytes = 0;
   }
   template <typename T>
   T* as() const { return reinterpret_cast<T*>(ptr); }

@@ -24,11 +24,14 @@
 
 namespace bm {
 
-int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
-                       int64_t P, double eps, uint32_t* adj, int32_t* cnt, const uint8_t* h_order,
-                       const std::vector<int32_t>& h_nrows, int64_t* stats,
-                       cudaStream_t stream);
 bool tc_supported(int64_t d);
+struct TcPrep;
+int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
+               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out);
+void tc_release(TcPrep* tp);
+int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, int32_t I0,
+              int32_t I1, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
+              cudaStream_t stream);
 
 namespace {
 
@@ -530,17 +533,258 @@ __global__ void pairwise_matrix_kernel(const double* __restrict__ X, int64_t d,
   }
 }
 
-// host-side batch description
-struct Batch {
-  int64_t k0, k1;  // element range [k0, k1)
-};
-
 }  // namespace
 
 // Exposed for the tcgen05 engine's verification path.
 int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, double eps,
                         uint32_t* adj, cudaStream_t stream) {
   return exact_build_adjacency(Xg, d, et, n_tp, eps, adj, stream);
+}
+
+// ---------------------------------------------------------------------------
+// One batch of elements resident on the device: gathered rows, per-row work
+// arrays, tables, and (tensor-core engine) the quantised planes. The bitmap
+// is produced per WINDOW of tile rows: the whole batch at once, or — for an
+// element whose bitmap exceeds the device budget — row
+// blocks [I0, I1) of a single-element batch, in two passes (counts for every
+// block, then components per block, recomputing the blocks that are not
+// resident). A window's bitmap holds tile pairs tri(I0,I0,T) ..
+// tri(I1,I1,T)-1 of the element's triangle; the window tables shift tp_off
+// so that every kernel addresses it unchanged.
+// ---------------------------------------------------------------------------
+struct BatchCtx {
+  cudaStream_t stream = nullptr;
+  int64_t d = 0;
+  double eps = 0.0;
+  int32_t min_pts = 1;
+  bool use_tc = false;
+  int64_t nb_el = 0, n_tp = 0, P = 0, n_entries = 0;
+  std::vector<int64_t> tp_off, offs;
+  std::vector<int32_t> pbase, nrows, ntiles;
+  std::vector<uint8_t> order;
+  Scratch tabs, xg, work;
+  ElemTables et{};
+  int32_t *cnt = nullptr, *par = nullptr, *bmin = nullptr, *lab = nullptr, *cmin = nullptr,
+          *head = nullptr;
+  int64_t* hscan = nullptr;
+  uint8_t* core = nullptr;
+  int64_t* d_offs = nullptr;
+  TcPrep* tc = nullptr;
+  BatchCtx() = default;
+  BatchCtx(const BatchCtx&) = delete;
+  ~BatchCtx() { tc_release(tc); }
+
+  int setup(const double* d_X, const int64_t* d_rows, const int64_t* h_offsets,
+            const uint8_t* h_order, int64_t k0, int64_t k1) {
+    nb_el = k1 - k0;
+    tp_off.assign(nb_el + 1, 0);
+    offs.assign(nb_el + 1, 0);
+    pbase.assign(nb_el + 1, 0);
+    nrows.assign(nb_el, 0);
+    ntiles.assign(nb_el, 0);
+    order.assign(nb_el, 0);
+    for (int64_t i = 0; i < nb_el; ++i) {
+      const int64_t k = k0 + i;
+      const int64_t nk = h_offsets[k + 1] - h_offsets[k];
+      const int64_t T = ceil_div(nk, kTile);
+      nrows[i] = (int32_t)nk;
+      ntiles[i] = (int32_t)T;
+      order[i] = h_order[k];
+      tp_off[i + 1] = tp_off[i] + T * (T + 1) / 2;
+      pbase[i + 1] = (int32_t)(pbase[i] + T * kTile);
+      offs[i] = h_offsets[k] - h_offsets[k0];
+    }
+    offs[nb_el] = h_offsets[k1] - h_offsets[k0];
+    n_tp = tp_off[nb_el];
+    P = pbase[nb_el];
+    n_entries = offs[nb_el];
+    if (n_entries == 0) return BM_OK;
+
+    const size_t tab_bytes = (nb_el + 1) * 8 * 2 + (nb_el + 1) * 4 * 3 + nb_el + 64;
+    BM_TRY(scratch_alloc(tabs, tab_bytes, stream));
+    char* tp = tabs.as<char>();
+    int64_t* d_tp_off = (int64_t*)tp;
+    d_offs = d_tp_off + nb_el + 1;
+    int32_t* d_pbase = (int32_t*)(d_offs + nb_el + 1);
+    int32_t* d_nrows = d_pbase + nb_el + 1;
+    int32_t* d_ntiles = d_nrows + nb_el + 1;
+    uint8_t* d_order = (uint8_t*)(d_ntiles + nb_el + 1);
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_tp_off, tp_off.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_offs, offs.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_pbase, pbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_nrows, nrows.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_ntiles, ntiles.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_order, order.data(), nb_el, cudaMemcpyHostToDevice, stream));
+    et = ElemTables{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, nb_el};
+
+    // gather rows (fp64, membership order, padded)
+    BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
+    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, d_rows + h_offsets[k0], d_offs,
+                                                          et, P, xg.as<double>());
+    BM_CHECK_LAUNCH();
+
+    // per-row work arrays (counts accumulate over the adjacency windows)
+    const size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
+    BM_TRY(scratch_alloc(work, wbytes, stream));
+    cnt = work.as<int32_t>();
+    par = cnt + P;
+    bmin = par + P;
+    lab = bmin + P;
+    cmin = lab + P;
+    head = cmin + P;
+    hscan = (int64_t*)(((uintptr_t)(head + P) + 15) & ~(uintptr_t)15);
+    core = (uint8_t*)(hscan + P + 1);
+    BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
+    if (use_tc) BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc));
+    return BM_OK;
+  }
+
+  // Tables addressing the bitmap of tile rows [I0, I1) of element 0 (I0 < 0:
+  // the whole batch). s keeps the shifted tp_off alive.
+  int window(int32_t I0, int32_t I1, ElemTables& etw, int64_t& n_tp_w, Scratch& s) {
+    if (I0 < 0) {
+      etw = et;
+      n_tp_w = n_tp;
+      return BM_OK;
+    }
+    BM_REQUIRE(nb_el == 1 && I0 < I1 && I1 <= ntiles[0], "bad row window [%d, %d)", I0, I1);
+    const int64_t T = ntiles[0];
+    auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
+    const int64_t h[2] = {-tri(I0), -tri(I0) + T * (T + 1) / 2};
+    BM_TRY(scratch_alloc(s, 16, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(s.ptr, h, 16, cudaMemcpyHostToDevice, stream));
+    etw = et;
+    etw.tp_off = s.as<int64_t>();
+    n_tp_w = tri(I1) - tri(I0);
+    return BM_OK;
+  }
+
+  // row-tile units of the window: diagonal tiles, then off-diagonal ranges
+  // of <= 32 tiles
+  int units(int32_t I0, int32_t I1, Scratch& s, int64_t& n_diag, int64_t& n_off) {
+    std::vector<TileUnit> hunits;
+    for (int64_t i = 0; i < nb_el; ++i) {
+      const int32_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? ntiles[i] : I1;
+      for (int32_t I = lo; I < hi; ++I) hunits.push_back({(int32_t)i, I, I, I + 1});
+    }
+    n_diag = (int64_t)hunits.size();
+    for (int64_t i = 0; i < nb_el; ++i) {
+      const int32_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? ntiles[i] : I1;
+      for (int32_t I = lo; I < hi; ++I)
+        for (int32_t J0 = I + 1; J0 < ntiles[i]; J0 += 32)
+          hunits.push_back({(int32_t)i, I, J0, std::min<int32_t>(J0 + 32, ntiles[i])});
+    }
+    n_off = (int64_t)hunits.size() - n_diag;
+    BM_TRY(scratch_alloc(s, std::max<size_t>(1, hunits.size()) * sizeof(TileUnit), stream));
+    if (!hunits.empty())
+      BM_CHECK_CUDA(cudaMemcpyAsync(s.ptr, hunits.data(), hunits.size() * sizeof(TileUnit),
+                                    cudaMemcpyHostToDevice, stream));
+    return BM_OK;
+  }
+
+  // Bits of the window into adj; counts added into cnt_acc (nullptr: the
+  // counts of this window were already taken).
+  int adjacency(int32_t I0, int32_t I1, uint32_t* adj, int32_t* cnt_acc, int64_t* stats) {
+    ElemTables etw;
+    int64_t n_tp_w = 0;
+    Scratch s_w;
+    BM_TRY(window(I0, I1, etw, n_tp_w, s_w));
+    if (use_tc) {
+      BM_TRY(tc_window(tc, xg.as<double>(), etw, n_tp_w, I0, I1, adj, cnt_acc, I0 >= 0, stats,
+                       stream));
+    } else {
+      BM_TRY(exact_build_adjacency(xg.as<double>(), d, etw, n_tp_w, eps, adj, stream));
+      if (cnt_acc) {
+        Scratch s_u;
+        int64_t n_diag = 0, n_off = 0;
+        BM_TRY(units(I0, I1, s_u, n_diag, n_off));
+        count_kernel<<<grid_for(n_diag + n_off, 1, 32), 128, 0, stream>>>(
+            adj, etw, s_u.as<TileUnit>(), n_diag + n_off, cnt_acc);
+        BM_CHECK_LAUNCH();
+      }
+      for (int64_t i = 0; i < nb_el; ++i) {
+        const int64_t nk = nrows[i];
+        const int64_t lo = I0 < 0 ? 0 : (int64_t)I0 * kTile;
+        const int64_t hi = I0 < 0 ? nk : std::min<int64_t>((int64_t)I1 * kTile, nk);
+        for (int64_t r = lo; r < hi; ++r) stats[0] += nk - 1 - r;  // distinct pairs (r, >r)
+      }
+    }
+    stats[3] += n_tp_w;
+    stats[4] = std::max<int64_t>(stats[4], n_tp_w * kTileWords * 4);
+    return BM_OK;
+  }
+
+  int init_core(const int32_t* counts, int32_t* par_out, int32_t* bmin_out) {
+    core_init_kernel<<<grid_for(P, 256), 256, 0, stream>>>(counts, et, P, min_pts, core, par_out,
+                                                           bmin_out);
+    BM_CHECK_LAUNCH();
+    return BM_OK;
+  }
+
+  // union-find over the core-core bits and border minima of the window
+  int components(int32_t I0, int32_t I1, const uint32_t* adj, int32_t* par_w, int32_t* bmin_w) {
+    ElemTables etw;
+    int64_t n_tp_w = 0;
+    Scratch s_w, s_u;
+    BM_TRY(window(I0, I1, etw, n_tp_w, s_w));
+    int64_t n_diag = 0, n_off = 0;
+    BM_TRY(units(I0, I1, s_u, n_diag, n_off));
+    const TileUnit* d_diag = s_u.as<TileUnit>();
+    components_kernel<true><<<grid_for(n_diag, 1, 32), 128, 0, stream>>>(adj, etw, d_diag, n_diag,
+                                                                         core, par_w, bmin_w);
+    BM_CHECK_LAUNCH();
+    compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
+    BM_CHECK_LAUNCH();
+    if (n_off > 0) {
+      components_kernel<false><<<grid_for(n_off, 1, 32), 128, 0, stream>>>(
+          adj, etw, d_diag + n_diag, n_off, core, par_w, bmin_w);
+      BM_CHECK_LAUNCH();
+    }
+    return BM_OK;
+  }
+
+  // canonical labels of every entry (element-relative cluster ids, -1 noise)
+  int finish(int32_t* par_w, const int32_t* bmin_w, int32_t* d_out, int32_t* h_ncl) {
+    label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par_w, bmin_w, lab, cmin);
+    BM_CHECK_LAUNCH();
+    head_kernel<<<grid_for(P, 256), 256, 0, stream>>>(P, lab, cmin, head);
+    BM_CHECK_LAUNCH();
+    BM_TRY(exclusive_scan_i32_to_i64(head, hscan, P, stream));
+    fill_total_kernel<<<1, 1, 0, stream>>>(hscan, head, P);  // hscan[P] = #heads
+    BM_CHECK_LAUNCH();
+    Scratch ncl_d;
+    BM_TRY(scratch_alloc(ncl_d, nb_el * 4, stream));
+    nclusters_kernel<<<(unsigned)ceil_div(nb_el, 128), 128, 0, stream>>>(et, hscan,
+                                                                          ncl_d.as<int32_t>());
+    BM_CHECK_LAUNCH();
+    output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(et, d_offs, n_entries, lab, cmin,
+                                                                hscan, d_out);
+    BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaMemcpyAsync(h_ncl, ncl_d.ptr, nb_el * 4, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    return BM_OK;
+  }
+};
+
+// Row windows of a T-tile triangle holding at most max_tiles tile pairs each
+// (every window has at least one tile row).
+std::vector<std::pair<int32_t, int32_t>> row_windows(int64_t T, int64_t max_tiles) {
+  std::vector<std::pair<int32_t, int32_t>> w;
+  int64_t I = 0;
+  while (I < T) {
+    int64_t acc = 0, J = I;
+    while (J < T && (J == I || acc + (T - J) <= max_tiles)) acc += T - J++;
+    w.push_back({(int32_t)I, (int32_t)J});
+    I = J;
+  }
+  return w;
+}
+
+int64_t row_window_cap() {
+  // B200MAP_WINDOW_TILES forces small windows (tests of the row-block path)
+  const char* e = getenv("B200MAP_WINDOW_TILES");
+  return e ? std::max<int64_t>(1, atoll(e)) : 0;
 }
 
 }  // namespace bm
@@ -582,193 +826,255 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     use_tc = tc_supported(d);
   }
 
-  // ---- batches bounded by the adjacency budget (bytes)
+  // ---- batches bounded by the device budget; an element whose bitmap alone
+  //      exceeds it is processed by itself in row windows
   size_t free_b = 0, total_b = 0;
   BM_CHECK_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double budget = 0.55 * (double)free_b;
+  const int64_t forced_cap = row_window_cap();
+  struct Batch {
+    int64_t k0, k1;
+    int64_t window_tiles;  // > 0: single huge element in row windows
+  };
   std::vector<Batch> batches;
   {
     int64_t k0 = 0;
     double acc = 0;
     for (int64_t k = 0; k < n_el; ++k) {
-      int64_t nk = h_offsets[k + 1] - h_offsets[k];
-      int64_t T = ceil_div(nk, kTile);
-      double bytes = (double)(T * (T + 1) / 2) * kTileWords * 4 +
-                     (double)T * kTile * (d * 8.0 + 4 * 4 + 1 + d * 2.0);
+      const int64_t nk = h_offsets[k + 1] - h_offsets[k];
+      const int64_t T = ceil_div(nk, kTile);
       BM_REQUIRE(T * kTile < (1ll << 31), "element %lld too large", (long long)k);
-      if (bytes > budget) {
-        set_error("element %lld (%lld rows) needs %.1f GB of adjacency; exceeds device budget "
-                  "%.1f GB (row-block sharding over several GPUs required)",
-                  (long long)k, (long long)nk, bytes / 1e9, budget / 1e9);
-        return BM_ERR_NOMEM;
+      const double row_bytes = (double)T * kTile * (d * 8.0 + 4 * 7 + 1 + 8 + d * 3.0);
+      const double bytes = (double)(T * (T + 1) / 2) * kTileWords * 4 + row_bytes;
+      if (bytes > budget || (forced_cap > 0 && T * (T + 1) / 2 > forced_cap)) {
+        if (k > k0) batches.push_back({k0, k, 0});
+        const double win_bytes = budget - row_bytes;
+        int64_t cap = (int64_t)(win_bytes / (kTileWords * 4.0));
+        if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
+        else if (cap < T) {
+          set_error("element %lld (%lld rows) leaves no room for one row window of its "
+                    "eps-graph (budget %.1f GB)", (long long)k, (long long)nk, budget / 1e9);
+          return BM_ERR_NOMEM;
+        }
+        batches.push_back({k, k + 1, cap});
+        k0 = k + 1;
+        acc = 0;
+        continue;
       }
       if (acc + bytes > budget && k > k0) {
-        batches.push_back({k0, k});
+        batches.push_back({k0, k, 0});
         k0 = k;
         acc = 0;
       }
       acc += bytes;
     }
-    batches.push_back({k0, n_el});
+    if (k0 < n_el) batches.push_back({k0, n_el, 0});
   }
 
   for (const Batch& bt : batches) {
-    const int64_t nb_el = bt.k1 - bt.k0;
-    std::vector<int64_t> tp_off(nb_el + 1, 0), offs(nb_el + 1, 0);
-    std::vector<int32_t> pbase(nb_el + 1, 0), nrows(nb_el), ntiles(nb_el);
-    std::vector<uint8_t> order(nb_el);
-    for (int64_t i = 0; i < nb_el; ++i) {
-      int64_t k = bt.k0 + i;
-      int64_t nk = h_offsets[k + 1] - h_offsets[k];
-      int64_t T = ceil_div(nk, kTile);
-      nrows[i] = (int32_t)nk;
-      ntiles[i] = (int32_t)T;
-      order[i] = h_order[k];
-      tp_off[i + 1] = tp_off[i] + T * (T + 1) / 2;
-      pbase[i + 1] = (int32_t)(pbase[i] + T * kTile);
-      offs[i] = h_offsets[k] - h_offsets[bt.k0];
-    }
-    offs[nb_el] = h_offsets[bt.k1] - h_offsets[bt.k0];
-    const int64_t n_tp = tp_off[nb_el];
-    const int64_t P = pbase[nb_el];
-    const int64_t n_entries = offs[nb_el];
-    if (n_entries == 0) continue;
-
-    // ---- device tables
-    Scratch tabs;
-    size_t tab_bytes = (nb_el + 1) * 8 * 2 + (nb_el + 1) * 4 * 3 + nb_el + 64;
-    BM_TRY(scratch_alloc(tabs, tab_bytes, stream));
-    char* tp = tabs.as<char>();
-    int64_t* d_tp_off = (int64_t*)tp;
-    int64_t* d_offs = d_tp_off + nb_el + 1;
-    int32_t* d_pbase = (int32_t*)(d_offs + nb_el + 1);
-    int32_t* d_nrows = d_pbase + nb_el + 1;
-    int32_t* d_ntiles = d_nrows + nb_el + 1;
-    uint8_t* d_order = (uint8_t*)(d_ntiles + nb_el + 1);
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_tp_off, tp_off.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_offs, offs.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_pbase, pbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_nrows, nrows.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_ntiles, ntiles.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(d_order, order.data(), nb_el, cudaMemcpyHostToDevice, stream));
-    ElemTables et{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, nb_el};
-
-    // ---- gather rows (fp64, membership order, padded)
-    cudaEvent_t evs = nullptr, ev2 = nullptr;
+    cudaEvent_t evs = nullptr, ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     BM_CHECK_CUDA(cudaEventCreate(&evs));
-    BM_CHECK_CUDA(cudaEventCreate(&ev2));
-    BM_CHECK_CUDA(cudaEventRecord(evs, stream));
-    Scratch xg;
-    BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
-    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(
-        d_X, d, d_rows + h_offsets[bt.k0], d_offs, et, P, xg.as<double>());
-    BM_CHECK_LAUNCH();
-
-    // ---- per-row work arrays (counts are filled by the adjacency stage for
-    //      the tensor-core engine, by count_kernel for the exact engine)
-    Scratch work;
-    size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
-    BM_TRY(scratch_alloc(work, wbytes, stream));
-    int32_t* cnt = work.as<int32_t>();
-    int32_t* par = cnt + P;
-    int32_t* bmin = par + P;
-    int32_t* lab = bmin + P;
-    int32_t* cmin = lab + P;
-    int32_t* head = cmin + P;
-    int64_t* hscan = (int64_t*)(((uintptr_t)(head + P) + 15) & ~(uintptr_t)15);
-    uint8_t* core = (uint8_t*)(hscan + P + 1);
-    BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
-    BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
-    // row-tile units: diagonal tiles, and off-diagonal ranges of <= 32 tiles
-    std::vector<TileUnit> hunits;
-    int64_t n_diag = 0;
-    for (int64_t i = 0; i < nb_el; ++i) {
-      for (int32_t I = 0; I < ntiles[i]; ++I) hunits.push_back({(int32_t)i, I, I, I + 1});
-    }
-    n_diag = (int64_t)hunits.size();
-    for (int64_t i = 0; i < nb_el; ++i)
-      for (int32_t I = 0; I < ntiles[i]; ++I)
-        for (int32_t J0 = I + 1; J0 < ntiles[i]; J0 += 32)
-          hunits.push_back({(int32_t)i, I, J0, std::min<int32_t>(J0 + 32, ntiles[i])});
-    const int64_t n_off = (int64_t)hunits.size() - n_diag;
-    Scratch s_units;
-    BM_TRY(scratch_alloc(s_units, std::max<size_t>(1, hunits.size()) * sizeof(TileUnit), stream));
-    if (!hunits.empty())
-      BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, hunits.data(), hunits.size() * sizeof(TileUnit),
-                                    cudaMemcpyHostToDevice, stream));
-    const TileUnit* d_diag = s_units.as<TileUnit>();
-    const TileUnit* d_off = d_diag + n_diag;
-
-    // ---- adjacency bitmap
-    Scratch adj;
-    BM_TRY(scratch_alloc(adj, (size_t)n_tp * kTileWords * 4, stream));
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     BM_CHECK_CUDA(cudaEventCreate(&ev0));
     BM_CHECK_CUDA(cudaEventCreate(&ev1));
-    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
-    if (use_tc) {
-      BM_TRY(tc_build_adjacency(xg.as<double>(), d, et, n_tp, P, eps, adj.as<uint32_t>(), cnt,
-                                order.data(), nrows, stats, stream));
-    } else {
-      BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, n_tp, eps, adj.as<uint32_t>(),
-                                   stream));
-      for (int64_t i = 0; i < nb_el; ++i) stats[0] += (int64_t)nrows[i] * (nrows[i] + 1) / 2;
-    }
-    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
-    stats[3] += n_tp;
-    stats[4] = std::max<int64_t>(stats[4], n_tp * kTileWords * 4);
-
-    // ---- counts, core, union-find, border
-    if (!use_tc) {
-      count_kernel<<<grid_for(n_diag + n_off, 1, 32), 128, 0, stream>>>(adj.as<uint32_t>(), et,
-                                                                       d_diag, n_diag + n_off, cnt);
-      BM_CHECK_LAUNCH();
-    }
-    core_init_kernel<<<grid_for(P, 256), 256, 0, stream>>>(cnt, et, P, min_pts, core, par, bmin);
-    BM_CHECK_LAUNCH();
-    components_kernel<true><<<grid_for(n_diag, 1, 32), 128, 0, stream>>>(adj.as<uint32_t>(), et,
-                                                                         d_diag, n_diag, core, par, bmin);
-    BM_CHECK_LAUNCH();
-    compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par, core, P);
-    BM_CHECK_LAUNCH();
-    if (n_off > 0)
-      components_kernel<false><<<grid_for(n_off, 1, 32), 128, 0, stream>>>(
-          adj.as<uint32_t>(), et, d_off, n_off, core, par, bmin);
-    BM_CHECK_LAUNCH();
-    label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par, bmin, lab, cmin);
-    BM_CHECK_LAUNCH();
-    head_kernel<<<grid_for(P, 256), 256, 0, stream>>>(P, lab, cmin, head);
-    BM_CHECK_LAUNCH();
-    BM_TRY(exclusive_scan_i32_to_i64(head, hscan, P, stream));
-    fill_total_kernel<<<1, 1, 0, stream>>>(hscan, head, P);  // hscan[P] = #heads
-    BM_CHECK_LAUNCH();
-    Scratch ncl_d;
-    BM_TRY(scratch_alloc(ncl_d, nb_el * 4, stream));
-    nclusters_kernel<<<(unsigned)ceil_div(nb_el, 128), 128, 0, stream>>>(et, hscan,
-                                                                          ncl_d.as<int32_t>());
-    BM_CHECK_LAUNCH();
-    output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(
-        et, d_offs, n_entries, lab, cmin, hscan, d_labels + h_offsets[bt.k0]);
-    BM_CHECK_LAUNCH();
-    BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(h_n_clusters + bt.k0, ncl_d.ptr, nb_el * 4,
-                                  cudaMemcpyDeviceToHost, stream));
-    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    BM_CHECK_CUDA(cudaEventCreate(&ev2));
+    struct EvGuard {
+      cudaEvent_t* e[4];
+      ~EvGuard() {
+        for (auto p : e) cudaEventDestroy(*p);
+      }
+    } evg{{&evs, &ev0, &ev1, &ev2}};
+    BM_CHECK_CUDA(cudaEventRecord(evs, stream));
+    BatchCtx bc;
+    bc.stream = stream;
+    bc.d = d;
+    bc.eps = eps;
+    bc.min_pts = min_pts;
+    bc.use_tc = use_tc;
+    BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1));
+    if (bc.n_entries == 0) continue;
+    int32_t* d_out = d_labels + h_offsets[bt.k0];
     float ms = 0.f, ms_pre = 0.f, ms_post = 0.f;
+    if (bt.window_tiles == 0) {
+      Scratch adj;
+      BM_TRY(scratch_alloc(adj, (size_t)bc.n_tp * kTileWords * 4, stream));
+      BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+      BM_TRY(bc.adjacency(-1, -1, adj.as<uint32_t>(), bc.cnt, stats));
+      BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+      BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
+      BM_TRY(bc.components(-1, -1, adj.as<uint32_t>(), bc.par, bc.bmin));
+      BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
+      BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
+    } else {
+      // pass 1: counts of every window (the last window's bits stay resident);
+      // pass 2: components of the resident window, then of the others with
+      // their bits recomputed (bit-identical: the decision is a pure function
+      // of the pair)
+      const auto wins = row_windows(bc.ntiles[0], bt.window_tiles);
+      int64_t max_w = 0;
+      for (auto& w : wins) {
+        const int64_t T = bc.ntiles[0];
+        auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
+        max_w = std::max<int64_t>(max_w, tri(w.second) - tri(w.first));
+      }
+      Scratch adj;
+      BM_TRY(scratch_alloc(adj, (size_t)max_w * kTileWords * 4, stream));
+      BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+      for (auto& w : wins) BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, stats));
+      BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+      BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
+      for (size_t i = wins.size(); i-- > 0;) {
+        if (i + 1 != wins.size())
+          BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, stats));
+        BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
+      }
+      BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
+      BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
+    }
+    BM_CHECK_CUDA(cudaEventSynchronize(ev2));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms_pre, evs, ev0));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms_post, ev1, ev2));
     stats[5] += (int64_t)(ms * 1e6);       // adjacency (distance) stage, ns on the launch stream
-    stats[6] += (int64_t)(ms_pre * 1e6);   // gather + setup
-    stats[7] += (int64_t)(ms_post * 1e6);  // counts, union-find, border, relabel
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    cudaEventDestroy(evs);
-    cudaEventDestroy(ev2);
+    stats[6] += (int64_t)(ms_pre * 1e6);   // gather + setup (+ quantisation)
+    stats[7] += (int64_t)(ms_post * 1e6);  // core, union-find, border, relabel (+ recomputed windows)
   }
   return BM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Row-block protocol for one huge element sharded over ranks:
+// every rank opens the element, takes the counts of its row windows,
+// all-reduce(sum) of counts, core + forest init, union-find of its windows,
+// forests merged on rank 0 (bm_merge_forest), all-reduce(min) of border
+// minima, labels on rank 0. The collectives stay in the host (NCCL through
+// torch.distributed); these entry points are the per-rank compute steps.
+// ---------------------------------------------------------------------------
+namespace bm {
+namespace {
+
+struct BigElement {
+  BatchCtx bc;
+  Scratch adj;
+  size_t adj_bytes = 0;
+  int32_t w0 = -1, w1 = -1;  // window whose bits are resident in adj
+  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  int bits(int32_t I0, int32_t I1, int32_t* cnt_acc) {
+    BM_REQUIRE(I0 >= 0 && I0 < I1 && I1 <= bc.ntiles[0], "bad row window [%d, %d)", I0, I1);
+    const int64_t T = bc.ntiles[0];
+    auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
+    const size_t need = (size_t)(tri(I1) - tri(I0)) * kTileWords * 4;
+    if (need > adj_bytes) {
+      adj.release();
+      BM_TRY(scratch_alloc(adj, need, bc.stream));
+      adj_bytes = need;
+    }
+    w0 = w1 = -1;
+    BM_TRY(bc.adjacency(I0, I1, adj.as<uint32_t>(), cnt_acc, stats));
+    w0 = I0;
+    w1 = I1;
+    return BM_OK;
+  }
+};
+
+__global__ void merge_forest_kernel(int32_t* __restrict__ par, const int32_t* __restrict__ other,
+                                    int64_t n) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int q = __ldg(other + p);
+    if (q != (int)p) uf_union(par, (int)p, q);
+  }
+}
+
+}  // namespace
+}  // namespace bm
+
+extern "C" int bm_big_open(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
+                           int64_t n_rows, double eps, int32_t min_pts, int order, int engine,
+                           void* stream, void** handle, int64_t* h_tiles) {
+  BM_REQUIRE(handle && h_tiles, "null output");
+  *handle = nullptr;
+  BM_REQUIRE(n >= 0 && d >= 1 && n_rows >= 1, "bad shapes");
+  BM_REQUIRE(d_X && d_rows, "null device pointer");
+  BM_REQUIRE(eps > 0.0, "eps must be positive");
+  BM_REQUIRE(min_pts >= 1, "min-pts must be >= 1");
+  BM_REQUIRE(order == BM_ORDER_SEQUENTIAL || order == BM_ORDER_PAIRWISE, "bad order flag");
+  BM_REQUIRE(engine == BM_ENGINE_AUTO || engine == BM_ENGINE_EXACT || engine == BM_ENGINE_TC,
+             "unknown engine %d", engine);
+  BM_REQUIRE(ceil_div(n_rows, kTile) * kTile < (1ll << 31), "element too large");
+  PwProgram probe;
+  BM_TRY(make_pw_program(d, &probe));
+  bool use_tc = engine == BM_ENGINE_TC || (engine == BM_ENGINE_AUTO && tc_supported(d));
+  BM_REQUIRE(!use_tc || tc_supported(d), "tensor-core engine does not support d=%lld",
+             (long long)d);
+  BigElement* be = new BigElement();
+  be->bc.stream = (cudaStream_t)stream;
+  be->bc.d = d;
+  be->bc.eps = eps;
+  be->bc.min_pts = min_pts;
+  be->bc.use_tc = use_tc;
+  const int64_t offs[2] = {0, n_rows};
+  const uint8_t ord = (uint8_t)order;
+  const int rc = be->bc.setup(d_X, d_rows, offs, &ord, 0, 1);
+  if (rc != BM_OK) {
+    delete be;
+    return rc;
+  }
+  *handle = be;
+  *h_tiles = be->bc.ntiles[0];
+  return BM_OK;
+}
+
+extern "C" int bm_big_counts(void* handle, int32_t I0, int32_t I1, int32_t* d_cnt) {
+  BM_REQUIRE(handle && d_cnt, "null argument");
+  return static_cast<BigElement*>(handle)->bits(I0, I1, d_cnt);
+}
+
+extern "C" int bm_big_init(void* handle, const int32_t* d_cnt, int32_t* d_par, int32_t* d_bmin) {
+  BM_REQUIRE(handle && d_cnt && d_par && d_bmin, "null argument");
+  return static_cast<BigElement*>(handle)->bc.init_core(d_cnt, d_par, d_bmin);
+}
+
+extern "C" int bm_big_components(void* handle, int32_t I0, int32_t I1, int32_t* d_par,
+                                 int32_t* d_bmin) {
+  BM_REQUIRE(handle && d_par && d_bmin, "null argument");
+  BigElement* be = static_cast<BigElement*>(handle);
+  if (be->w0 != I0 || be->w1 != I1) BM_TRY(be->bits(I0, I1, nullptr));
+  return be->bc.components(I0, I1, be->adj.as<uint32_t>(), d_par, d_bmin);
+}
+
+extern "C" int bm_big_labels(void* handle, int32_t* d_par, const int32_t* d_bmin,
+                             int32_t* d_labels, int32_t* h_n_clusters) {
+  BM_REQUIRE(handle && d_par && d_bmin && d_labels && h_n_clusters, "null argument");
+  BigElement* be = static_cast<BigElement*>(handle);
+  return be->bc.finish(d_par, d_bmin, d_labels, h_n_clusters);
+}
+
+extern "C" int bm_big_stats(void* handle, int64_t* h_stats) {
+  BM_REQUIRE(handle && h_stats, "null argument");
+  BigElement* be = static_cast<BigElement*>(handle);
+  for (int i = 0; i < 8; ++i) h_stats[i] = be->stats[i];
+  return BM_OK;
+}
+
+extern "C" int bm_big_close(void* handle) {
+  if (handle) {
+    BigElement* be = static_cast<BigElement*>(handle);
+    cudaStream_t s = be->bc.stream;
+    delete be;
+    BM_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  return BM_OK;
+}
+
+extern "C" int bm_merge_forest(int32_t* d_par, const int32_t* d_other, int64_t n, void* stream) {
+  BM_REQUIRE(n >= 0, "bad size");
+  if (n == 0) return BM_OK;
+  BM_REQUIRE(d_par && d_other, "null device pointer");
+  merge_forest_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(d_par, d_other, n);
+  BM_CHECK_LAUNCH();
+  return BM_OK;
+}
 
 extern "C" int bm_pairwise_distances(const double* d_X, int64_t n, int64_t d,
                                      const int64_t* d_rows, int64_t n_rows, int order,

@@ -1013,12 +1013,27 @@ inline unsigned grid_cap(int64_t n, int threads, int per_sm) {
 
 bool tc_supported(int64_t d) { return d >= 32 && d <= 256; }
 
-int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, int64_t P,
-                       double eps, uint32_t* adj, int32_t* cnt, const uint8_t* h_order,
-                       const std::vector<int32_t>& h_nrows, int64_t* stats,
-                       cudaStream_t stream) {
-  (void)h_order;
-  const int64_t n_el = et.n_el;
+// Per-batch state of the tensor-core engine: quantised limb planes, row
+// norms, per-tile error bounds and element thresholds. Built once per batch
+// and reused by every row window (a huge element is processed in windows of
+// tile rows, twice: counts, then components).
+struct TcPrep {
+  int64_t d = 0, P = 0, n_el = 0, n_tiles = 0, kpad = 0;
+  int nkc = 0;
+  double eps = 0.0;
+  std::vector<int32_t> nrows;
+  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw;
+  int32_t* d_tile_elem = nullptr;
+  int32_t* d_tbase = nullptr;
+  double* tile_u = nullptr;
+  double* a_in = nullptr;
+  double* a_out = nullptr;
+  CUtensorMap qmap;
+};
+
+int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
+               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out) {
+  *out = nullptr;
   const int64_t kpad = ceil_div(d, kKC) * kKC;
   const int nkc = (int)(kpad / kKC);
   BM_REQUIRE(nkc >= 1 && nkc <= 2, "tensor-core engine supports d <= 256");
@@ -1026,65 +1041,124 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   BM_TRY(make_pw_program(d, &prog));
   BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog_tc, &prog, sizeof(prog), 0,
                                         cudaMemcpyHostToDevice, stream));
-
-  // ---- host tables: tile -> element, element tile base, work units
+  TcPrep* tp = new TcPrep();
+  struct Guard {
+    TcPrep*& p;
+    ~Guard() { delete p; }
+  } guard{tp};
+  const int64_t n_el = et.n_el;
+  tp->d = d;
+  tp->P = P;
+  tp->n_el = n_el;
+  tp->kpad = kpad;
+  tp->nkc = nkc;
+  tp->eps = eps;
+  tp->nrows = h_nrows;
   const int64_t n_tiles = P / kTile;
+  tp->n_tiles = n_tiles;
   std::vector<int32_t> tile_elem(n_tiles), tbase(n_el + 1, 0);
-  std::vector<Unit> units;
   for (int64_t k = 0; k < n_el; ++k) {
     const int64_t T = ceil_div(h_nrows[k], kTile);
     tbase[k + 1] = (int32_t)(tbase[k] + T);
     for (int64_t t = 0; t < T; ++t) tile_elem[tbase[k] + t] = (int32_t)k;
-    for (int64_t I = 0; I < T; ++I)
-      for (int64_t b0 = I; b0 < T; b0 += kUnitB)
-        units.push_back({(int32_t)k, (int32_t)I, (int32_t)b0,
-                         (int32_t)std::min<int64_t>(b0 + kUnitB, T)});
   }
-  const int64_t n_units = (int64_t)units.size();
-  if (n_units == 0) return BM_OK;
-
-  // ---- device buffers
-  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_units, s_q, s_cnt;
-  BM_TRY(scratch_alloc(s_tab, (n_tiles + n_el + 1) * 4 + 16, stream));
-  int32_t* d_tile_elem = s_tab.as<int32_t>();
-  int32_t* d_tbase = d_tile_elem + n_tiles;
-  BM_CHECK_CUDA(cudaMemcpyAsync(d_tile_elem, tile_elem.data(), n_tiles * 4,
+  BM_TRY(scratch_alloc(tp->s_tab, (n_tiles + n_el + 1) * 4 + 16, stream));
+  tp->d_tile_elem = tp->s_tab.as<int32_t>();
+  tp->d_tbase = tp->d_tile_elem + n_tiles;
+  BM_CHECK_CUDA(cudaMemcpyAsync(tp->d_tile_elem, tile_elem.data(), n_tiles * 4,
                                 cudaMemcpyHostToDevice, stream));
-  BM_CHECK_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), (n_el + 1) * 4, cudaMemcpyHostToDevice,
+  BM_CHECK_CUDA(cudaMemcpyAsync(tp->d_tbase, tbase.data(), (n_el + 1) * 4, cudaMemcpyHostToDevice,
                                 stream));
-  BM_TRY(scratch_alloc(s_mm, (size_t)n_tiles * d * 16, stream));
-  double* tmin = s_mm.as<double>();
+  BM_TRY(scratch_alloc(tp->s_mm, (size_t)n_tiles * d * 16, stream));
+  double* tmin = tp->s_mm.as<double>();
   double* tmax = tmin + n_tiles * d;
-  BM_TRY(scratch_alloc(s_cs, (size_t)(n_el * d + n_el) * 8, stream));
-  double* center = s_cs.as<double>();
+  BM_TRY(scratch_alloc(tp->s_cs, (size_t)(n_el * d + n_el) * 8, stream));
+  double* center = tp->s_cs.as<double>();
   double* scale = center + n_el * d;
-  BM_TRY(scratch_alloc(s_pl, (size_t)3 * P * kpad, stream));
-  BM_TRY(scratch_alloc(s_nq, (size_t)P * 12, stream));
-  BM_TRY(scratch_alloc(s_te, (size_t)n_tiles * 8, stream));
-  BM_CHECK_CUDA(cudaMemsetAsync(s_te.ptr, 0, n_tiles * 8, stream));
-  BM_TRY(scratch_alloc(s_units, n_units * sizeof(Unit), stream));
-  BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, units.data(), n_units * sizeof(Unit),
-                                cudaMemcpyHostToDevice, stream));
+  BM_TRY(scratch_alloc(tp->s_pl, (size_t)3 * P * kpad, stream));
+  BM_TRY(scratch_alloc(tp->s_nq, (size_t)P * 12, stream));
+  BM_TRY(scratch_alloc(tp->s_te, (size_t)n_tiles * 8, stream));
+  BM_CHECK_CUDA(cudaMemsetAsync(tp->s_te.ptr, 0, n_tiles * 8, stream));
 
-  tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, d_tile_elem, n_tiles, tmin,
-                                                            tmax);
+  tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, tp->d_tile_elem, n_tiles,
+                                                            tmin, tmax);
   BM_CHECK_LAUNCH();
-  elem_scale_kernel<<<(unsigned)n_el, 256, 0, stream>>>(d, et, d_tbase, tmin, tmax, center,
+  elem_scale_kernel<<<(unsigned)n_el, 256, 0, stream>>>(d, et, tp->d_tbase, tmin, tmax, center,
                                                         scale);
   BM_CHECK_LAUNCH();
   quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
-      Xg, d, kpad, et, P, center, scale, s_pl.as<int8_t>(), s_nq.as<int64_t>(),
-      reinterpret_cast<int32_t*>(s_nq.as<int64_t>() + P),
-      s_te.as<unsigned long long>());
+      Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
+      reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>());
   BM_CHECK_LAUNCH();
+  BM_TRY(make_qmap(&tp->qmap, tp->s_pl.ptr, P, kpad));
 
-  CUtensorMap qmap;
-  BM_TRY(make_qmap(&qmap, s_pl.ptr, P, kpad));
+  const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
+  BM_TRY(scratch_alloc(tp->s_thr, (size_t)(n_tiles + 2 * n_el) * 8, stream));
+  tp->tile_u = tp->s_thr.as<double>();
+  tp->a_in = tp->tile_u + n_tiles;
+  tp->a_out = tp->a_in + n_el;
+  thresholds_prep_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n_tiles, n_el), 256), 256, 0,
+                           stream>>>(tp->s_te.as<unsigned long long>(), tp->d_tile_elem, n_tiles,
+                                     scale, n_el, eps, gamma, tp->tile_u, tp->a_in, tp->a_out);
+  BM_CHECK_LAUNCH();
+  // the per-point error bounds are folded into tile_u; min/max/centre are
+  // no longer needed
+  *out = tp;
+  tp = nullptr;  // disarm the guard
+  return BM_OK;
+}
+
+void tc_release(TcPrep* tp) { delete tp; }
+
+__global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                                  int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (src[i]) dst[i] += src[i];
+}
+
+// Adjacency bits and eps-neighbour counts of the tile rows [I0, I1) of every
+// element (I0 < 0: all rows). `et` addresses the bitmap window being written
+// (for a window, tp_off[k] = -tri(I0, I0, T)); n_tp = tiles in that window.
+// accumulate: add the window's counts into cnt instead of overwriting it;
+// cnt == nullptr: the counts of this window are not wanted (recomputed window).
+int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, int32_t I0,
+              int32_t I1, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
+              cudaStream_t stream) {
+  const int64_t n_el = tp->n_el, P = tp->P, d = tp->d;
+  const int nkc = tp->nkc;
+  std::vector<Unit> units;
+  int64_t pairs = 0;
+  for (int64_t k = 0; k < n_el; ++k) {
+    const int64_t T = ceil_div(tp->nrows[k], kTile);
+    const int64_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? T : std::min<int64_t>(I1, T);
+    for (int64_t I = lo; I < hi; ++I) {
+      for (int64_t b0 = I; b0 < T; b0 += kUnitB)
+        units.push_back({(int32_t)k, (int32_t)I, (int32_t)b0,
+                         (int32_t)std::min<int64_t>(b0 + kUnitB, T)});
+      // unordered distinct pairs of this tile row (its rows against every later row)
+      const int64_t r0 = I * kTile, r1 = std::min<int64_t>(r0 + kTile, tp->nrows[k]);
+      if (r1 > r0) {
+        const int64_t m = r1 - r0, rest = tp->nrows[k] - r1;
+        pairs += m * (m - 1) / 2 + m * rest;
+      }
+    }
+  }
+  const int64_t n_units = (int64_t)units.size();
+  if (n_units == 0) return BM_OK;
+  Scratch s_units, s_q, s_cnt, s_tt;
+  BM_TRY(scratch_alloc(s_units, n_units * sizeof(Unit), stream));
+  BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, units.data(), n_units * sizeof(Unit),
+                                cudaMemcpyHostToDevice, stream));
+  int32_t* cnt_run = cnt;
+  if (accumulate || !cnt) {  // window counts go to a private buffer first
+    if (!tp->s_cntw.ptr) BM_TRY(scratch_alloc(tp->s_cntw, (size_t)P * 4, stream));
+    cnt_run = tp->s_cntw.as<int32_t>();
+  }
 
   // ---- MMA pass (re-run with a larger recheck queue on overflow)
-  int64_t pairs = 0;
-  for (int64_t k = 0; k < n_el; ++k) pairs += (int64_t)h_nrows[k] * h_nrows[k];
-  unsigned long long qcap = std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 5000));
+  unsigned long long qcap =
+      std::max<unsigned long long>(1ull << 20, (unsigned long long)(2 * pairs / 5000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
   const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;
@@ -1096,41 +1170,30 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
-  Scratch s_thr;
-  BM_TRY(scratch_alloc(s_thr, (size_t)(n_tiles + 2 * n_el) * 8, stream));
-  double* tile_u = s_thr.as<double>();
-  double* a_in = tile_u + n_tiles;
-  double* a_out = a_in + n_el;
-  thresholds_prep_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n_tiles, n_el), 256), 256, 0,
-                           stream>>>(s_te.as<unsigned long long>(), d_tile_elem, n_tiles, scale,
-                                     n_el, eps, gamma, tile_u, a_in, a_out);
-  BM_CHECK_LAUNCH();
-  Scratch s_tt;
   BM_TRY(scratch_alloc(s_tt, (size_t)n_tp * sizeof(TileThr), stream));
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
     BM_TRY(scratch_alloc(s_q, qcap * sizeof(int2), stream));
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
-    BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, (size_t)P * 4, stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));
     TcParams prm{};
     prm.et = et;
     prm.units = s_units.as<Unit>();
     prm.n_units = n_units;
-    prm.nq = s_nq.as<int64_t>();
-    prm.cq = reinterpret_cast<const int32_t*>(s_nq.as<int64_t>() + P);
-    prm.tile_u = tile_u;
-    prm.tbase = d_tbase;
-    prm.a_in = a_in;
-    prm.a_out = a_out;
+    prm.nq = tp->s_nq.as<int64_t>();
+    prm.cq = reinterpret_cast<const int32_t*>(tp->s_nq.as<int64_t>() + P);
+    prm.tile_u = tp->tile_u;
+    prm.tbase = tp->d_tbase;
+    prm.a_in = tp->a_in;
+    prm.a_out = tp->a_out;
     const double lmax = (double)((1 << kLimb) - 1);
-    prm.ll2 = 2.0 * lmax * lmax * (double)kpad;                           // 2 L.L
-    prm.a3max = (double)(2 << kLimb) * 2.0 * lmax * lmax * (double)kpad;  // 2^(b+1) A3
+    prm.ll2 = 2.0 * lmax * lmax * (double)tp->kpad;                           // 2 L.L
+    prm.a3max = (double)(2 << kLimb) * 2.0 * lmax * lmax * (double)tp->kpad;  // 2^(b+1) A3
     prm.nkc = nkc;
     prm.adj = adj;
-    prm.cnt = cnt;
+    prm.cnt = cnt_run;
     prm.queue = s_q.as<int2>();
-    prm.planes = s_pl.as<uint8_t>();
+    prm.planes = tp->s_pl.as<uint8_t>();
     prm.P = P;
     prm.qcount = d_cnt;
     prm.qcap = qcap;
@@ -1149,9 +1212,9 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
     }
     const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
     if (nkc == 1)
-      tc_adjacency_kernel<1><<<grid, kThreads, smem, stream>>>(qmap, prm);
+      tc_adjacency_kernel<1><<<grid, kThreads, smem, stream>>>(tp->qmap, prm);
     else
-      tc_adjacency_kernel<2><<<grid, kThreads, smem, stream>>>(qmap, prm);
+      tc_adjacency_kernel<2><<<grid, kThreads, smem, stream>>>(tp->qmap, prm);
     BM_CHECK_LAUNCH();
     BM_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
@@ -1183,8 +1246,12 @@ int tc_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_
   }
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
-    recheck_kernel<<<grid_cap(nrec, kRcWarps * 32, 8), kRcWarps * 32, 0, stream>>>(Xg, d, et, s_q.as<int2>(), nrec,
-                                                                eps, adj, cnt, d_cnt + 1);
+    recheck_kernel<<<grid_cap(nrec, kRcWarps * 32, 8), kRcWarps * 32, 0, stream>>>(
+        Xg, d, et, s_q.as<int2>(), nrec, tp->eps, adj, cnt_run, d_cnt + 1);
+    BM_CHECK_LAUNCH();
+  }
+  if (accumulate && cnt) {
+    add_counts_kernel<<<grid_cap(P, 256, 8), 256, 0, stream>>>(cnt, cnt_run, P);
     BM_CHECK_LAUNCH();
   }
   stats[0] += pairs;

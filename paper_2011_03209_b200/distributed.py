@@ -7,6 +7,13 @@ instances, so the work partitions with no data-path collective; the single
 exchange is the gather of per-entry cluster labels to the rank that builds
 nodes and edges.
 
+An element too large for LPT to balance (n_k^2 above 1/world of the total)
+or for one device's memory is instead split by ROW BLOCKS of its triangular
+eps-graph: ranks take tile-row windows of equal tile
+area, all-reduce(sum) the eps-neighbour counts, union their windows'
+core-core bits locally, and rank 0 merges the forests and the all-reduced
+(min) border choices into the labels (`rowblock_cluster`).
+
 Every rank holds X and evaluates the (cheap, HBM-bound) lens and cover
 itself, so memberships are identical on all ranks without communication.
 Elements are assigned by LPT on the pair work n_k^2 (largest first onto the
@@ -88,6 +95,100 @@ def gather_labels(labels_local, ncl_local, elems: list, parts: list, offsets: np
     return full[:total], ncl
 
 
+def tri_rows(T: int, I: int) -> int:
+    """Tile pairs (I', J >= I') in tile rows [0, I) of a T-tile triangle."""
+    return I * T - I * (I - 1) // 2
+
+
+def area_windows(T: int, world: int) -> list:
+    """Tile-row windows [I0, I1) per rank with (nearly) equal tile area;
+    empty windows (I0 == I1) when T < world."""
+    total = tri_rows(T, T)
+    cuts = [0]
+    I = 0
+    for r in range(1, world):
+        target = total * r / world
+        while I < T and tri_rows(T, I + 1) <= target:
+            I += 1
+        if I < T and tri_rows(T, I + 1) - target < target - tri_rows(T, I):
+            I += 1  # nearest cut: every window is within one tile row of its share
+        cuts.append(max(I, cuts[-1]))
+    cuts.append(T)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def split_window(I0: int, I1: int, T: int, max_tiles: int) -> list:
+    """Sub-windows of [I0, I1) holding at most max_tiles tile pairs (>= 1 row each)."""
+    out = []
+    I = I0
+    while I < I1:
+        J, acc = I, 0
+        while J < I1 and (J == I or acc + (T - J) <= max_tiles):
+            acc += T - J
+            J += 1
+        out.append((I, J))
+        I = J
+    return out
+
+
+def big_elements(sizes, world: int) -> list:
+    """Elements whose pair work exceeds 1/world of the total: row-blocked."""
+    if world <= 1:
+        return []
+    work = [float(s) ** 2 for s in sizes]
+    total = sum(work)
+    return [k for k, w in enumerate(work) if total > 0 and w > total / world]
+
+
+def _all_gather(t, world: int, dist):
+    import torch
+
+    if dist.get_backend() == "nccl":
+        out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t)
+        return out
+    chunks = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(chunks, t)
+    return torch.stack(chunks)
+
+
+def rowblock_cluster(be, rank: int, world: int, dist, max_tiles: int, merge_forest):
+    """DBSCAN of one element split over ranks by tile-row windows.
+
+    `be` provides the per-rank steps (engine.BigElement on a GPU; a numpy
+    model in the CPU tests): counts -> all_reduce(sum) -> init -> components
+    (resident window first) -> forests gathered and merged on rank 0,
+    all_reduce(min) of border minima -> labels on rank 0. Returns
+    (labels, n_clusters) on rank 0, (None, None) elsewhere. The result is the
+    element's unique DBSCAN labelling, identical for every world size."""
+    I0, I1 = area_windows(be.tiles, world)[rank]
+    wins = split_window(I0, I1, be.tiles, max_tiles) if I1 > I0 else []
+    cnt = be.zeros()
+    for w in wins:
+        be.counts(w[0], w[1], cnt)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    par, bmin = be.zeros(), be.zeros()
+    be.init(cnt, par, bmin)
+    for w in reversed(wins):  # the last window's bits are still resident
+        be.components(w[0], w[1], par, bmin)
+    dist.all_reduce(bmin, op=dist.ReduceOp.MIN)
+    forests = _all_gather(par, world, dist)
+    if rank != 0:
+        return None, None
+    for r in range(1, world):
+        merge_forest(par, forests[r])
+    return be.labels(par, bmin)
+
+
+def device_window_tiles(device, d: int, rows: int) -> int:
+    """Largest row window (tile pairs) that fits next to the element's rows."""
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(device)
+    row_bytes = rows * (d * 11.0 + 64)
+    return max(1, int((0.55 * free - row_bytes) / 2048))
+
+
 def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=None,
                       engine: int = 0):
     """Sharded hot path. Returns a DeviceGraph on rank 0 and None elsewhere."""
@@ -108,7 +209,8 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     sizes = np.diff(offsets)
     budget = effective_mem_budget() if budget_bytes is None else budget_bytes
     orders = element_orders(sizes, params.strategy, budget)
-    parts = lpt_partition(sizes, world)
+    big = big_elements(sizes, world)
+    parts = lpt_partition([0 if k in big else s for k, s in enumerate(sizes)], world)
     mine = parts[rank]
     ranges, loc = pack_local(offsets, mine)
     st = np.zeros(8, dtype=np.int64)
@@ -122,6 +224,16 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
         ncl_loc = np.zeros(len(mine), dtype=np.int32)
     labels, ncl = gather_labels(labels_loc, ncl_loc, mine, parts, offsets, len(sizes), rank,
                                 world, dist, X.device)
+    for k in big:  # every rank takes an equal tile area of each big element
+        a, b = int(offsets[k]), int(offsets[k + 1])
+        with eng.BigElement(X, rows[a:b], params.eps, params.min_pts, int(orders[k]),
+                            engine) as be:
+            cap = device_window_tiles(X.device, X.shape[1], be.padded)
+            lab_k, ncl_k = rowblock_cluster(be, rank, world, dist, cap, eng.merge_forest)
+            st = st + be.stats()
+        if rank == 0:
+            labels[a:b] = lab_k
+            ncl[k] = ncl_k
     if rank != 0:
         return None, st
     node_rows, node_off, n_nodes = eng.group_nodes(rows, offsets, labels, ncl)

@@ -95,6 +95,72 @@ def cluster(X: torch.Tensor, rows: torch.Tensor, offsets: np.ndarray, eps: float
     return labels[: int(offsets[-1])], ncl[:n_el], stats
 
 
+class BigElement:
+    """Row-block protocol handle for ONE cover element sharded over ranks
+    (include/b200map.h bm_big_*). Arrays cnt/par/bmin hold
+    `padded` int32 entries; every call runs on the stream current at open."""
+
+    TILE = 128
+
+    def __init__(self, X: torch.Tensor, rows: torch.Tensor, eps: float, min_pts: int, order: int,
+                 engine: int = _native.ENGINE_AUTO):
+        n, d = X.shape
+        self._lib = _native.load()
+        self._h = ctypes.c_void_p()
+        tiles = ctypes.c_int64(0)
+        self.device = X.device
+        self.n_rows = int(rows.numel())
+        rc = self._lib.bm_big_open(P(X), n, d, P(rows), self.n_rows, ctypes.c_double(float(eps)),
+                                   int(min_pts), int(order), int(engine), stream_ptr(X.device),
+                                   ctypes.byref(self._h), ctypes.byref(tiles))
+        _native.check(rc, "big element open")
+        self.tiles = int(tiles.value)
+        self.padded = self.tiles * self.TILE
+
+    def zeros(self) -> torch.Tensor:
+        return torch.zeros(self.padded, dtype=torch.int32, device=self.device)
+
+    def counts(self, I0: int, I1: int, cnt: torch.Tensor) -> None:
+        _native.check(self._lib.bm_big_counts(self._h, int(I0), int(I1), P(cnt)), "big counts")
+
+    def init(self, cnt: torch.Tensor, par: torch.Tensor, bmin: torch.Tensor) -> None:
+        _native.check(self._lib.bm_big_init(self._h, P(cnt), P(par), P(bmin)), "big init")
+
+    def components(self, I0: int, I1: int, par: torch.Tensor, bmin: torch.Tensor) -> None:
+        _native.check(self._lib.bm_big_components(self._h, int(I0), int(I1), P(par), P(bmin)),
+                      "big components")
+
+    def labels(self, par: torch.Tensor, bmin: torch.Tensor):
+        out = torch.empty(max(self.n_rows, 1), dtype=torch.int32, device=self.device)
+        ncl = np.zeros(1, dtype=np.int32)
+        _native.check(self._lib.bm_big_labels(self._h, P(par), P(bmin), P(out), P(ncl)),
+                      "big labels")
+        return out[: self.n_rows], int(ncl[0])
+
+    def stats(self) -> np.ndarray:
+        st = np.zeros(8, dtype=np.int64)
+        _native.check(self._lib.bm_big_stats(self._h, P(st)), "big stats")
+        return st
+
+    def close(self) -> None:
+        if self._h:
+            _native.check(self._lib.bm_big_close(self._h), "big close")
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def merge_forest(par: torch.Tensor, other: torch.Tensor) -> None:
+    """par := union of the union-find forests par and other (same length)."""
+    rc = _native.load().bm_merge_forest(P(par), P(other), int(par.numel()),
+                                        stream_ptr(par.device))
+    _native.check(rc, "merge forest")
+
+
 def group_nodes(rows: torch.Tensor, offsets: np.ndarray, labels: torch.Tensor,
                 n_clusters: np.ndarray):
     """Node row lists in (element, cluster) order (nerve.py:84-101)."""

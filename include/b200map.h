@@ -60,6 +60,9 @@ int64_t bm_launch_count(void);
 int bm_release_scratch(void);
 /* Number of visible CUDA devices (for the host-side GPU-count knob). */
 int bm_device_count(int* out);
+/* Free bytes on the current device, counting what the library's stream-ordered
+ * pool retains unused (sizes the row windows of bm_big_*). */
+int bm_device_free_bytes(int64_t* out);
 
 /* ---- K1: lens (filters.py:133-140, evaluate) --------------------------------
  * out[i] = X[i,col]                         (BM_LENS_COLUMN, filters.py:135-136)

@@ -45,6 +45,7 @@ _SIGNATURES = {
     "bm_launch_count": (ctypes.c_int64, []),
     "bm_release_scratch": (ctypes.c_int, []),
     "bm_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "bm_device_free_bytes": (ctypes.c_int, [_vp]),
     "bm_lens_f64": (ctypes.c_int, [ctypes.c_int, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp]),
     "bm_normalize_f64": (ctypes.c_int, [ctypes.c_int, _vp, _c_i64, _c_i64, _vp, _vp]),
     "bm_membership_count": (ctypes.c_int, [_vp, _c_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),

@@ -47,6 +47,24 @@ static void retain_pool_once() {
   cudaGetLastError();
 }
 
+int device_free_bytes(size_t* free_b) {
+  size_t total = 0;
+  BM_CHECK_CUDA(cudaMemGetInfo(free_b, &total));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) ==
+            cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      *free_b += (size_t)(reserved - used);  // retained by the pool, reusable
+  }
+  cudaGetLastError();
+  return BM_OK;
+}
+
 void release_pool() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -236,6 +254,14 @@ int bm_release_scratch(void) {
 }
 
 const char* bm_last_error(void) { return bm::get_error(); }
+
+int bm_device_free_bytes(int64_t* out) {
+  BM_REQUIRE(out, "null output");
+  size_t f = 0;
+  BM_TRY(bm::device_free_bytes(&f));
+  *out = (int64_t)f;
+  return BM_OK;
+}
 
 int bm_device_count(int* out) {
   int n = 0;

@@ -77,6 +77,9 @@ struct Scratch {
 
 int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream);
 
+// Free device memory including what the stream-ordered pool retains unused.
+int device_free_bytes(size_t* free_b);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Number of SMs on the current device (cached per device).

@@ -768,16 +768,20 @@ struct BatchCtx {
 };
 
 // Row windows of a T-tile triangle holding at most max_tiles tile pairs each
-// (every window has at least one tile row).
+// (every window has at least one tile row), in ascending row order. Built
+// from the bottom so that the LAST window — the one whose bits stay resident
+// between the two passes — is the full one and the recomputed remainder is
+// as small as possible.
 std::vector<std::pair<int32_t, int32_t>> row_windows(int64_t T, int64_t max_tiles) {
   std::vector<std::pair<int32_t, int32_t>> w;
-  int64_t I = 0;
-  while (I < T) {
-    int64_t acc = 0, J = I;
-    while (J < T && (J == I || acc + (T - J) <= max_tiles)) acc += T - J++;
-    w.push_back({(int32_t)I, (int32_t)J});
-    I = J;
+  int64_t I1 = T;
+  while (I1 > 0) {
+    int64_t acc = 0, I = I1;
+    while (I > 0 && (I == I1 || acc + (T - (I - 1)) <= max_tiles)) acc += T - --I;
+    w.push_back({(int32_t)I, (int32_t)I1});
+    I1 = I;
   }
+  std::reverse(w.begin(), w.end());
   return w;
 }
 
@@ -828,8 +832,8 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
 
   // ---- batches bounded by the device budget; an element whose bitmap alone
   //      exceeds it is processed by itself in row windows
-  size_t free_b = 0, total_b = 0;
-  BM_CHECK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  size_t free_b = 0;
+  BM_TRY(device_free_bytes(&free_b));
   const double budget = 0.55 * (double)free_b;
   const int64_t forced_cap = row_window_cap();
   struct Batch {
@@ -848,8 +852,10 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       const double bytes = (double)(T * (T + 1) / 2) * kTileWords * 4 + row_bytes;
       if (bytes > budget || (forced_cap > 0 && T * (T + 1) / 2 > forced_cap)) {
         if (k > k0) batches.push_back({k0, k, 0});
-        const double win_bytes = budget - row_bytes;
-        int64_t cap = (int64_t)(win_bytes / (kTileWords * 4.0));
+        // the window may use most of the free memory: besides the rows it
+        // needs ~8 B per tile pair for thresholds and the recheck queue
+        const double win_bytes = 0.85 * (double)free_b - row_bytes - (4ll << 30);
+        int64_t cap = (int64_t)(win_bytes / (kTileWords * 4.0 + 8.0));
         if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
         else if (cap < T) {
           set_error("element %lld (%lld rows) leaves no room for one row window of its "

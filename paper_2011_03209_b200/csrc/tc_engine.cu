@@ -1158,7 +1158,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
 
   // ---- MMA pass (re-run with a larger recheck queue on overflow)
   unsigned long long qcap =
-      std::max<unsigned long long>(1ull << 20, (unsigned long long)(2 * pairs / 5000));
+      std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 10000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
   const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;

@@ -184,9 +184,14 @@ def device_window_tiles(device, d: int, rows: int) -> int:
     """Largest row window (tile pairs) that fits next to the element's rows."""
     import torch
 
-    free, _ = torch.cuda.mem_get_info(device)
+    from . import _native
+
+    with torch.cuda.device(device):
+        free = np.zeros(1, dtype=np.int64)
+        _native.check(_native.load().bm_device_free_bytes(_native.ptr(free)), "free bytes")
+        free = int(free[0])
     row_bytes = rows * (d * 11.0 + 64)
-    return max(1, int((0.55 * free - row_bytes) / 2048))
+    return max(1, int((0.85 * free - row_bytes - (4 << 30)) / 2056))
 
 
 def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=None,

@@ -77,6 +77,10 @@ struct Scratch {
 
 int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream);
 
+// Stable sort of (keys, vals) by the low key_bits bits of keys (LSD radix,
+// graph.cu); result in place. vals may be null.
+int sort_pairs_u64(uint64_t* keys, int64_t* vals, int64_t n, int key_bits, cudaStream_t s);
+
 // Free device memory including what the stream-ordered pool retains unused.
 int device_free_bytes(size_t* free_b);
 

@@ -29,8 +29,9 @@ struct TcPrep;
 int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
                const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out);
 void tc_release(TcPrep* tp);
-int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, int32_t I0,
-              int32_t I1, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
+int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
+              int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
+              int64_t pairs, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
               cudaStream_t stream);
 
 namespace {
@@ -38,29 +39,321 @@ namespace {
 __constant__ PwProgram c_prog;
 
 // ---------------------------------------------------------------------------
-// gather: Xg[p] = X[rows[e]] (zero for pads). One warp per padded row.
+// gather: Xg[p] = X[rows[ent[p]]] (zero for pads). One warp per padded row.
 // ---------------------------------------------------------------------------
 __global__ void gather_kernel(const double* __restrict__ X, int64_t d,
-                              const int64_t* __restrict__ rows,
-                              const int64_t* __restrict__ offsets,  // n_el+1 (batch-relative)
+                              const int64_t* __restrict__ rows,  // batch entries
                               ElemTables et, int64_t P, double* __restrict__ Xg) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
        p += (int64_t)gridDim.x * wpb) {
-    int64_t a = 0, b = et.n_el;
-    while (b - a > 1) {
-      int64_t mid = (a + b) >> 1;
-      if (et.pbase[mid] <= p) a = mid; else b = mid;
-    }
-    int64_t i = p - et.pbase[a];
+    const int e = et.ent[p];
     double* dst = Xg + p * d;
-    if (i < et.nrows[a]) {
-      const double* src = X + rows[offsets[a] + i] * d;
+    if (e >= 0) {
+      const double* src = X + rows[e] * d;
       for (int64_t c = lane; c < d; c += 32) dst[c] = src[c];
     } else {
       for (int64_t c = lane; c < d; c += 32) dst[c] = 0.0;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Spatial grouping inside an element (performance only — any order gives the
+// same result, the order-dependent rules run on entry indices). Each entry
+// picks the nearest of S evenly spaced seed entries of its element over the
+// first kGroupDims dims (fp32); a stable sort by (element, seed) makes row
+// tiles compact, so tile pairs of far-apart groups can be pruned.
+// ---------------------------------------------------------------------------
+constexpr int kGroupSeeds = 64;
+constexpr int kGroupDims = 64;
+constexpr int kGroupMinRows = 3 * kTile;  // smaller elements keep their order
+
+struct GroupItem {
+  int32_t k, e0, e1, pad;  // element, entries [e0, e1) (batch-relative)
+};
+
+__global__ void __launch_bounds__(128)
+group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                    const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
+                    uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+  __shared__ float sd[kGroupDims][kGroupSeeds];  // seed coordinates, [dim][seed]
+  const GroupItem it = items[blockIdx.x];
+  const int64_t ek = offs[it.k], nk = offs[it.k + 1] - ek;
+  const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
+  const int D = d < kGroupDims ? (int)d : kGroupDims;
+  for (int i = threadIdx.x; i < kGroupDims * kGroupSeeds; i += blockDim.x) {
+    const int dim = i / kGroupSeeds, j = i % kGroupSeeds;
+    float v = 3.0e38f;  // unused seeds are far away
+    if (j < S && dim < D) v = (float)X[rows[ek + (j * nk) / S] * d + dim];
+    else if (j < S) v = 0.0f;
+    sd[dim][j] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int e = it.e0 + (threadIdx.x >> 5); e < it.e1; e += blockDim.x >> 5) {
+    const double* x = X + rows[e] * d;
+    const float x0 = lane < D ? (float)x[lane] : 0.0f;
+    const float x1 = lane + 32 < D ? (float)x[lane + 32] : 0.0f;
+    float d0 = 0.0f, d1 = 0.0f;  // seeds lane, lane + 32
+    for (int dim = 0; dim < D; ++dim) {
+      const float xv = __shfl_sync(0xffffffffu, dim < 32 ? x0 : x1, dim & 31);
+      const float a = xv - sd[dim][lane], b = xv - sd[dim][lane + 32];
+      d0 = fmaf(a, a, d0);
+      d1 = fmaf(b, b, d1);
+    }
+    if (lane >= S) d0 = 3.0e38f;
+    if (lane + 32 >= S) d1 = 3.0e38f;
+    float best = d0;
+    int bi = lane;
+    if (d1 < best) {
+      best = d1;
+      bi = lane + 32;
+    }
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      keys[e] = ((uint64_t)it.k << 7) | (uint64_t)bi;
+      vals[e] = e;
+    }
+  }
+}
+
+// identity order (key = element) for the entries of elements with fewer than
+// min_rows rows
+__global__ void group_identity_kernel(const int64_t* __restrict__ offs, int64_t n_el,
+                                      int64_t n_entries, int64_t min_rows,
+                                      uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = n_el;
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (offs[mid] <= e) a = mid; else b = mid;
+    }
+    if (offs[a + 1] - offs[a] < min_rows) {
+      keys[e] = (uint64_t)a << 7;
+      vals[e] = e;
+    }
+  }
+}
+
+// sorted entries -> ent (per padded row) and inv (per entry)
+__global__ void perm_kernel(const int64_t* __restrict__ sorted, const int64_t* __restrict__ offs,
+                            ElemTables et, int64_t P, int32_t* __restrict__ ent,
+                            int32_t* __restrict__ inv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = et.n_el;
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (et.pbase[mid] <= p) a = mid; else b = mid;
+    }
+    const int64_t i = p - et.pbase[a];
+    if (i < et.nrows[a]) {
+      const int e = (int)sorted[offs[a] + i];
+      ent[p] = e;
+      inv[e] = (int32_t)p;
+    } else {
+      ent[p] = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile geometry and pruning. Per 128-row tile: a centre c (the fp64 mean of
+// its rows — any point works) and a radius r >= max |x - c| (fp64 norm plus
+// a relative margin far above its rounding error). For I != J, every pair of
+// rows is at true distance >= |c_I - c_J| - r_I - r_J, and the reference's
+// fp64 distance is within a factor (1 +- gamma) of the true one, so
+//   (|c_I - c_J| (1 - 1e-12) - r_I - r_J) (1 - gamma) > eps
+// proves that no pair of the tile pair is an eps-neighbour. NaN/inf rows make
+// the bound NaN and keep the tile pair.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+tile_geom_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+                 const int32_t* __restrict__ tile_elem, double* __restrict__ cen,
+                 double* __restrict__ rad) {
+  const int64_t t = blockIdx.x;
+  const int k = tile_elem[t];
+  const int64_t p0 = t * kTile;
+  const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
+  double* c = cen + t * d;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < valid; ++r) s += Xg[(p0 + r) * d + j];
+    c[j] = s / (double)valid;
+  }
+  __syncthreads();
+  __shared__ double wmax[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double m = 0.0;
+  bool nan = false;
+  for (int r = w; r < valid; r += 8) {
+    double s = 0.0;
+    for (int64_t j = lane; j < d; j += 32) {
+      const double df = Xg[(p0 + r) * d + j] - c[j];
+      s += df * df;
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (s == s) m = fmax(m, sqrt(s));
+    else nan = true;  // NaN poisons the radius (keeps every tile pair)
+  }
+  if (lane == 0) wmax[w] = nan ? __longlong_as_double(0x7ff8000000000000ll) : m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = 0.0;
+    bool any_nan = false;
+    for (int i = 0; i < 8; ++i) {
+      if (wmax[i] == wmax[i]) mm = fmax(mm, wmax[i]);
+      else any_nan = true;
+    }
+    rad[t] = any_nan ? __longlong_as_double(0x7ff8000000000000ll) : mm * (1.0 + 1e-12) + 1e-300;
+  }
+}
+
+constexpr int kPruneB = 64;   // 64 x 64 tile pairs per CTA (4 x 4 per thread)
+constexpr int kPruneDC = 32;  // centre dims staged per step
+
+struct PruneBlock {
+  int32_t k, bi, bj, pad;
+};
+
+// flags[g] = 1 if dense tile pair g of the batch must be computed
+__global__ void __launch_bounds__(256)
+tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
+                  const PruneBlock* __restrict__ blocks, const double* __restrict__ cen,
+                  const double* __restrict__ rad, double eps, double gamma,
+                  int32_t* __restrict__ flags) {
+  __shared__ double sa[kPruneDC][kPruneB + 1], sb[kPruneDC][kPruneB + 1];
+  const PruneBlock pbk = blocks[blockIdx.x];
+  const int k = pbk.k, T = et.ntiles[k];
+  const int64_t tb = tbase[k];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = pbk.bi * kPruneB, j0 = pbk.bj * kPruneB;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t c0 = 0; c0 < d; c0 += kPruneDC) {
+    const int dc = (d - c0) < kPruneDC ? (int)(d - c0) : kPruneDC;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPruneB * kPruneDC; i += blockDim.x) {
+      const int t = i / kPruneDC, c = i % kPruneDC;
+      const bool okc = c < dc;
+      sa[c][t] = (okc && i0 + t < T) ? cen[(tb + i0 + t) * d + c0 + c] : 0.0;
+      sb[c][t] = (okc && j0 + t < T) ? cen[(tb + j0 + t) * d + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < dc; ++c) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sa[c][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sb[c][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double df = av[a] - bv[b];
+          acc[a][b] = fma(df, df, acc[a][b]);
+        }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int I = i0 + ty + 16 * a, J = j0 + tx + 16 * b;
+      if (I >= T || J >= T || J < I) continue;
+      int keep = 1;
+      if (I != J) {
+        const double lb =
+            (sqrt(acc[a][b]) * (1.0 - 1e-12) - rad[tb + I] - rad[tb + J]) * (1.0 - gamma);
+        keep = lb > eps ? 0 : 1;
+      }
+      flags[et.tp_off[k] + tri_index(I, J, T)] = keep;
+    }
+}
+
+__global__ void fill_ones_kernel(int32_t* __restrict__ f, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    f[i] = 1;
+}
+
+// Per row tile rt = tbase[k] + I (one warp): its kept tiles into the list at
+// pos[g] (ascending J), the row's first slot and the distinct row pairs of
+// its kept tiles.
+__global__ void emit_tiles_kernel(ElemTables et, const int32_t* __restrict__ row_elem,
+                                  const int32_t* __restrict__ tbase, int64_t n_rt,
+                                  const int32_t* __restrict__ flags,
+                                  const int64_t* __restrict__ pos, TileRef* __restrict__ tiles,
+                                  int64_t* __restrict__ row_first, int64_t* __restrict__ row_pairs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t rt = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); rt < n_rt;
+       rt += (int64_t)gridDim.x * wpb) {
+    const int k = row_elem[rt];
+    const int I = (int)(rt - tbase[k]);
+    const int T = et.ntiles[k], nk = et.nrows[k];
+    const int64_t g0 = et.tp_off[k] + tri_index(I, I, T);
+    const int64_t vI = min(kTile, nk - I * kTile);
+    int64_t pr = 0;
+    for (int J = I + lane; J < T; J += 32) {
+      const int64_t g = g0 + (J - I);
+      if (flags[g]) {
+        tiles[pos[g]] = TileRef{k, I, J, 0};
+        const int64_t vJ = min(kTile, nk - J * kTile);
+        pr += J == I ? vI * (vI - 1) / 2 : vI * vJ;
+      }
+    }
+    for (int o = 16; o; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    if (lane == 0) {
+      row_first[rt] = pos[g0];
+      row_pairs[rt] = pr;
+    }
+  }
+}
+
+// unit counts per row tile (from the kept slots of consecutive rows)
+__global__ void unit_counts_kernel(const int64_t* __restrict__ row_first, int64_t n_rt,
+                                   int64_t* __restrict__ n_off, int64_t* __restrict__ n_tc) {
+  for (int64_t rt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rt < n_rt;
+       rt += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = row_first[rt + 1] - row_first[rt];
+    n_off[rt] = (c - 1 + 31) / 32;
+    n_tc[rt] = (c + 31) / 32;
+  }
+}
+
+// units of every row tile: diagonal unit rt; off-diagonal units at
+// off_pos[rt] (slots after the diagonal); tensor-core units at tc_pos[rt]
+__global__ void emit_units_kernel(const int32_t* __restrict__ row_elem,
+                                  const int32_t* __restrict__ tbase, int64_t n_rt,
+                                  const int64_t* __restrict__ row_first,
+                                  const int64_t* __restrict__ off_pos,
+                                  const int64_t* __restrict__ tc_pos, TileUnit* __restrict__ diag,
+                                  TileUnit* __restrict__ off, TileUnit* __restrict__ tcu) {
+  for (int64_t rt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rt < n_rt;
+       rt += (int64_t)gridDim.x * blockDim.x) {
+    const int k = row_elem[rt];
+    const int I = (int)(rt - tbase[k]);
+    const int64_t f = row_first[rt];
+    const int c = (int)(row_first[rt + 1] - f);
+    diag[rt] = TileUnit{k, I, (int32_t)f, 1};
+    int64_t o = off_pos[rt];
+    for (int j = 1; j < c; j += 32) off[o++] = TileUnit{k, I, (int32_t)(f + j), min(32, c - j)};
+    o = tc_pos[rt];
+    for (int j = 0; j < c; j += 32) tcu[o++] = TileUnit{k, I, (int32_t)(f + j), min(32, c - j)};
   }
 }
 
@@ -170,15 +463,16 @@ __device__ __forceinline__ void stage_rows(double* S, const double* __restrict__
 template <int DEPTH>
 __global__ void __launch_bounds__(256, 1)
 adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, double eps,
-                       uint32_t* __restrict__ adj, int64_t tile0) {
+                       const TileRef* __restrict__ tiles, uint32_t* __restrict__ adj,
+                       int64_t tile0) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + kKC * kLd;
   __shared__ uint32_t bits[kTile * 4];
 
-  const int64_t g = tile0 + blockIdx.x;
-  int k, I, J;
-  decode_tile(et, g, k, I, J);
+  const int64_t g = tile0 + blockIdx.x;  // slot
+  const TileRef tr = tiles[g];
+  const int k = tr.k, I = tr.I, J = tr.J;
   const int n_k = et.nrows[k];
   const int64_t pb = et.pbase[k];
   const int mode = et.order[k];
@@ -263,16 +557,18 @@ adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128)
 count_kernel(const uint32_t* __restrict__ adj, ElemTables et, const TileUnit* __restrict__ units,
-             int64_t n_units, int32_t* __restrict__ cnt) {
+             const TileRef* __restrict__ tiles, int64_t slot0, int64_t n_units,
+             int32_t* __restrict__ cnt) {
   __shared__ uint32_t bits[kTileWords];
   for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     const TileUnit un = units[u];
-    const int64_t pb = et.pbase[un.k], tpk = et.tp_off[un.k], T = et.ntiles[un.k];
+    const int64_t pb = et.pbase[un.k];
     int rc = 0;
-    for (int J = un.J0; J < un.J1; ++J) {
-      const int64_t g = tpk + tri_index(un.I, J, T);
+    for (int t = 0; t < un.cnt; ++t) {
+      const int64_t g = un.off + t;
+      const int J = tiles[g].J;
       __syncthreads();
-      const uint4 w = reinterpret_cast<const uint4*>(adj + g * kTileWords)[threadIdx.x];
+      const uint4 w = reinterpret_cast<const uint4*>(adj + (g - slot0) * kTileWords)[threadIdx.x];
       reinterpret_cast<uint4*>(bits)[threadIdx.x] = w;
       rc += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
       if (J != un.I) {
@@ -325,9 +621,9 @@ __device__ __forceinline__ bool lunion(int* lp, int a, int b) {
 template <bool DIAG>
 __global__ void __launch_bounds__(128)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
-                  const TileUnit* __restrict__ units, int64_t n_units,
-                  const uint8_t* __restrict__ core, int32_t* __restrict__ par,
-                  int32_t* __restrict__ bmin) {
+                  const TileUnit* __restrict__ units, const TileRef* __restrict__ tiles,
+                  int64_t slot0, int64_t n_units, const uint8_t* __restrict__ core,
+                  int32_t* __restrict__ par, int32_t* __restrict__ bmin) {
   __shared__ uint32_t bits[kTileWords];
   __shared__ int groot[2 * kTile];  // global root of each tile node (-1: not core)
   __shared__ int lp[2 * kTile];     // local union-find over tile nodes
@@ -337,7 +633,7 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
   for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     const TileUnit un = units[u];
     const int k = un.k, I = un.I;
-    const int64_t pb = et.pbase[k], tpk = et.tp_off[k], T = et.ntiles[k];
+    const int64_t pb = et.pbase[k];
     const int nk = et.nrows[k];
     const int pI = (int)(pb + I * kTile);
     // row side once per unit (stale roots later only cost redundant unions)
@@ -348,11 +644,13 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
       const unsigned bi = __ballot_sync(0xffffffffu, ci);
       if ((t & 31) == 0) coreI[t >> 5] = bi;
     }
-    for (int J = un.J0; J < un.J1; ++J) {
-      const int64_t g = tpk + tri_index(I, J, T);
+    for (int s = 0; s < un.cnt; ++s) {
+      const int64_t g = un.off + s;
+      const int J = tiles[g].J;
       const int pJ = (int)(pb + J * kTile);
       __syncthreads();
-      reinterpret_cast<uint4*>(bits)[t] = reinterpret_cast<const uint4*>(adj + g * kTileWords)[t];
+      reinterpret_cast<uint4*>(bits)[t] =
+          reinterpret_cast<const uint4*>(adj + (g - slot0) * kTileWords)[t];
       const bool cj = DIAG ? ci : (bool)core[pJ + t];
       if (!DIAG) {
         const unsigned bj = __ballot_sync(0xffffffffu, cj);
@@ -380,29 +678,29 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
           }
         }
       }
-      // --- border: non-core row r -> smallest core column
+      // --- border: non-core row r -> its core neighbour of smallest ENTRY
       if (!ci && r < nk - I * kTile) {
+        const int cb = DIAG ? pI : pJ;
+        int best = kNoCore;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
-          if (m) {
+          while (m) {
             const int c = w * 32 + __ffs(m) - 1;
-            const int cand = (DIAG ? pI : pJ) + c;
-            if (cand < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, cand);
-            break;
+            m &= m - 1;
+            best = min(best, et.ent[cb + c]);
           }
         }
+        if (best < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, best);
       }
-      // --- border: non-core column c -> smallest core row (off-diagonal only)
+      // --- border: non-core column c -> its core row of smallest entry (off-diagonal only)
       if (!DIAG && !cj && t < nk - J * kTile) {
         const int c = t, wd = c >> 5, sh = c & 31;
-        for (int rr = 0; rr < kTile; ++rr) {
-          if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u)) {
-            const int cand = pI + rr;
-            if (cand < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, cand);
-            break;
-          }
-        }
+        int best = kNoCore;
+        for (int rr = 0; rr < kTile; ++rr)
+          if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u))
+            best = min(best, et.ent[pI + rr]);
+        if (best < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, best);
       }
       __syncthreads();
       // --- propagate local merges to the global forest
@@ -425,32 +723,37 @@ __global__ void compress_kernel(int32_t* __restrict__ par, const uint8_t* __rest
     if (core[p]) par[p] = uf_find(par, (int)p);
 }
 
-// root label per padded index (-1 noise), and cluster min member via atomicMin
+// root label per padded index (-1 noise); cluster's smallest ENTRY via atomicMin
 __global__ void label_kernel(ElemTables et, int64_t P, const uint8_t* __restrict__ core,
                              int32_t* __restrict__ par, const int32_t* __restrict__ bmin,
-                             int32_t* __restrict__ lab, int32_t* __restrict__ cmin) {
+                             const int32_t* __restrict__ inv, int32_t* __restrict__ lab,
+                             int32_t* __restrict__ cmin) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     int root = -1;
     if (core[p]) root = uf_find(par, (int)p);
-    else if (bmin[p] != kNoCore) root = uf_find(par, bmin[p]);
+    else if (bmin[p] != kNoCore) root = uf_find(par, inv[bmin[p]]);
     lab[p] = root;
-    if (root >= 0) atomicMin(cmin + root, (int)p);
+    if (root >= 0) atomicMin(cmin + root, et.ent[p]);
   }
 }
 
-__global__ void head_kernel(int64_t P, const int32_t* __restrict__ lab,
-                            const int32_t* __restrict__ cmin, int32_t* __restrict__ head) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int r = lab[p];
-    head[p] = (r >= 0 && cmin[r] == (int)p) ? 1 : 0;
+// head[e] = entry e is the smallest member of its cluster
+__global__ void head_kernel(int64_t n_entries, const int32_t* __restrict__ inv,
+                            const int32_t* __restrict__ lab, const int32_t* __restrict__ cmin,
+                            int32_t* __restrict__ head) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = lab[inv[e]];
+    head[e] = (r >= 0 && cmin[r] == (int)e) ? 1 : 0;
   }
 }
 
+// cluster rank of every entry inside its element (clusters ordered by their
+// smallest entry, clustering.py:192-197), -1 for noise
 __global__ void output_kernel(ElemTables et, const int64_t* __restrict__ offsets,
-                              int64_t n_entries, const int32_t* __restrict__ lab,
-                              const int32_t* __restrict__ cmin,
+                              int64_t n_entries, const int32_t* __restrict__ inv,
+                              const int32_t* __restrict__ lab, const int32_t* __restrict__ cmin,
                               const int64_t* __restrict__ hscan, int32_t* __restrict__ out) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -459,23 +762,19 @@ __global__ void output_kernel(ElemTables et, const int64_t* __restrict__ offsets
       int64_t mid = (a + b) >> 1;
       if (offsets[mid] <= e) a = mid; else b = mid;
     }
-    // skip empty elements sharing the same offset: the owning element is the
-    // last one whose offset <= e and that has rows (offsets strictly increase
-    // across non-empty elements)
-    const int64_t p = et.pbase[a] + (e - offsets[a]);
-    const int r = lab[p];
-    out[e] = r >= 0 ? (int32_t)(hscan[cmin[r]] - hscan[et.pbase[a]]) : -1;
+    const int r = lab[inv[e]];
+    out[e] = r >= 0 ? (int32_t)(hscan[cmin[r]] - hscan[offsets[a]]) : -1;
   }
 }
 
-__global__ void fill_total_kernel(int64_t* hs, const int32_t* hd, int64_t P) {
-  hs[P] = (P > 0 ? hs[P - 1] + hd[P - 1] : 0);
+__global__ void fill_total_kernel(int64_t* hs, const int32_t* hd, int64_t n) {
+  hs[n] = (n > 0 ? hs[n - 1] + hd[n - 1] : 0);
 }
 
-__global__ void nclusters_kernel(ElemTables et, const int64_t* __restrict__ hscan,
-                                 int32_t* __restrict__ ncl) {
+__global__ void nclusters_kernel(ElemTables et, const int64_t* __restrict__ offsets,
+                                 const int64_t* __restrict__ hscan, int32_t* __restrict__ ncl) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < et.n_el) ncl[k] = (int32_t)(hscan[et.pbase[k + 1]] - hscan[et.pbase[k]]);
+  if (k < et.n_el) ncl[k] = (int32_t)(hscan[offsets[k + 1]] - hscan[offsets[k]]);
 }
 
 inline unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
@@ -487,8 +786,8 @@ inline unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
 }
 
 template <int DEPTH>
-int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, double eps,
-                       uint32_t* adj, cudaStream_t stream) {
+int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
+                       int64_t n_tiles, double eps, uint32_t* adj, cudaStream_t stream) {
   static bool attr_done = false;  // per process; attribute is per function
   if (!attr_done) {
     BM_CHECK_CUDA(cudaFuncSetAttribute(adjacency_exact_kernel<DEPTH>,
@@ -497,27 +796,28 @@ int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, int64_
     attr_done = true;
   }
   const int64_t kMaxGrid = 1ll << 30;
-  for (int64_t t0 = 0; t0 < n_tp; t0 += kMaxGrid) {
-    int64_t nb = std::min<int64_t>(kMaxGrid, n_tp - t0);
-    adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(Xg, d, et, eps, adj,
-                                                                            t0);
+  for (int64_t t0 = 0; t0 < n_tiles; t0 += kMaxGrid) {
+    int64_t nb = std::min<int64_t>(kMaxGrid, n_tiles - t0);
+    adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(Xg, d, et, eps,
+                                                                            tiles, adj, t0);
     BM_CHECK_LAUNCH();
   }
   return BM_OK;
 }
 
-int exact_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
-                          double eps, uint32_t* adj, cudaStream_t stream) {
+int exact_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
+                          int64_t n_tiles, double eps, uint32_t* adj, cudaStream_t stream) {
+  if (n_tiles == 0) return BM_OK;
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
   BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
                                         stream));
   switch (prog.depth) {
-    case 1: return launch_exact_depth<1>(Xg, d, et, n_tp, eps, adj, stream);
-    case 2: return launch_exact_depth<2>(Xg, d, et, n_tp, eps, adj, stream);
-    case 3: return launch_exact_depth<3>(Xg, d, et, n_tp, eps, adj, stream);
-    case 4: return launch_exact_depth<4>(Xg, d, et, n_tp, eps, adj, stream);
-    default: return launch_exact_depth<kMaxStack>(Xg, d, et, n_tp, eps, adj, stream);
+    case 1: return launch_exact_depth<1>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
+    case 2: return launch_exact_depth<2>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
+    case 3: return launch_exact_depth<3>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
+    case 4: return launch_exact_depth<4>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
+    default: return launch_exact_depth<kMaxStack>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
   }
 }
 
@@ -535,37 +835,49 @@ __global__ void pairwise_matrix_kernel(const double* __restrict__ X, int64_t d,
 
 }  // namespace
 
-// Exposed for the tcgen05 engine's verification path.
-int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp, double eps,
-                        uint32_t* adj, cudaStream_t stream) {
-  return exact_build_adjacency(Xg, d, et, n_tp, eps, adj, stream);
+// ---------------------------------------------------------------------------
+// One batch of elements resident on the device: the grouping permutation,
+// gathered rows, per-row work arrays, tables, the pruned tile list and (tensor-
+// core engine) the quantised planes. Bits are produced per WINDOW of tile rows:
+// the whole batch at once, or — for an element whose bitmap exceeds the device
+// budget — row blocks [I0, I1) of a single-element batch,
+// in two passes (counts for every block, then components per block,
+// recomputing the blocks that are not resident). A window is a contiguous run
+// of the kept-tile list (sorted by element, row tile, column tile); its slots
+// are renumbered from 0 and adj[slot] holds the bits.
+// ---------------------------------------------------------------------------
+struct WindowBufs {
+  const TileRef* tiles = nullptr;  // the batch's full kept list (absolute slots)
+  const TileUnit *diag = nullptr, *off = nullptr, *tcu = nullptr;
+  int64_t slot0 = 0, n_tiles = 0, n_diag = 0, n_off = 0, n_tc = 0, pairs = 0;
+};
+
+bool prune_enabled(int64_t d) {
+  const char* e = getenv("B200MAP_NO_PRUNE");  // tests: identity order, every tile pair
+  return !(e && e[0] == '1') && d <= 512;
 }
 
-// ---------------------------------------------------------------------------
-// One batch of elements resident on the device: gathered rows, per-row work
-// arrays, tables, and (tensor-core engine) the quantised planes. The bitmap
-// is produced per WINDOW of tile rows: the whole batch at once, or — for an
-// element whose bitmap exceeds the device budget — row
-// blocks [I0, I1) of a single-element batch, in two passes (counts for every
-// block, then components per block, recomputing the blocks that are not
-// resident). A window's bitmap holds tile pairs tri(I0,I0,T) ..
-// tri(I1,I1,T)-1 of the element's triangle; the window tables shift tp_off
-// so that every kernel addresses it unchanged.
-// ---------------------------------------------------------------------------
 struct BatchCtx {
   cudaStream_t stream = nullptr;
   int64_t d = 0;
   double eps = 0.0;
   int32_t min_pts = 1;
   bool use_tc = false;
-  int64_t nb_el = 0, n_tp = 0, P = 0, n_entries = 0;
+  int64_t nb_el = 0, n_tp = 0, P = 0, n_entries = 0, n_rt = 0;
   std::vector<int64_t> tp_off, offs;
-  std::vector<int32_t> pbase, nrows, ntiles;
+  std::vector<int32_t> pbase, nrows, ntiles, tbase;
   std::vector<uint8_t> order;
-  Scratch tabs, xg, work;
+  // kept tile pairs (device list sorted by (k, I, J)) and, per global row
+  // tile rt = tbase[k] + I, host copies of: first slot (n_rt+1 entries, last =
+  // n_kept), first off-diagonal / tensor-core unit (n_rt+1), row pairs
+  int64_t n_kept = 0;
+  std::vector<int64_t> row_first, off_pos, tc_pos, row_pairs;
+  Scratch tabs, xg, work, perm, s_tiles, s_units;
+  TileRef* d_tiles = nullptr;
+  TileUnit *d_diag = nullptr, *d_off = nullptr, *d_tcu = nullptr;
   ElemTables et{};
   int32_t *cnt = nullptr, *par = nullptr, *bmin = nullptr, *lab = nullptr, *cmin = nullptr,
-          *head = nullptr;
+          *head = nullptr, *ent = nullptr, *inv = nullptr;
   int64_t* hscan = nullptr;
   uint8_t* core = nullptr;
   int64_t* d_offs = nullptr;
@@ -575,11 +887,12 @@ struct BatchCtx {
   ~BatchCtx() { tc_release(tc); }
 
   int setup(const double* d_X, const int64_t* d_rows, const int64_t* h_offsets,
-            const uint8_t* h_order, int64_t k0, int64_t k1) {
+            const uint8_t* h_order, int64_t k0, int64_t k1, int64_t* stats) {
     nb_el = k1 - k0;
     tp_off.assign(nb_el + 1, 0);
     offs.assign(nb_el + 1, 0);
     pbase.assign(nb_el + 1, 0);
+    tbase.assign(nb_el + 1, 0);
     nrows.assign(nb_el, 0);
     ntiles.assign(nb_el, 0);
     order.assign(nb_el, 0);
@@ -592,15 +905,17 @@ struct BatchCtx {
       order[i] = h_order[k];
       tp_off[i + 1] = tp_off[i] + T * (T + 1) / 2;
       pbase[i + 1] = (int32_t)(pbase[i] + T * kTile);
+      tbase[i + 1] = (int32_t)(tbase[i] + T);
       offs[i] = h_offsets[k] - h_offsets[k0];
     }
     offs[nb_el] = h_offsets[k1] - h_offsets[k0];
     n_tp = tp_off[nb_el];
     P = pbase[nb_el];
+    n_rt = tbase[nb_el];
     n_entries = offs[nb_el];
     if (n_entries == 0) return BM_OK;
 
-    const size_t tab_bytes = (nb_el + 1) * 8 * 2 + (nb_el + 1) * 4 * 3 + nb_el + 64;
+    const size_t tab_bytes = (nb_el + 1) * 8 * 2 + (nb_el + 1) * 4 * 4 + nb_el + 64;
     BM_TRY(scratch_alloc(tabs, tab_bytes, stream));
     char* tp = tabs.as<char>();
     int64_t* d_tp_off = (int64_t*)tp;
@@ -608,22 +923,66 @@ struct BatchCtx {
     int32_t* d_pbase = (int32_t*)(d_offs + nb_el + 1);
     int32_t* d_nrows = d_pbase + nb_el + 1;
     int32_t* d_ntiles = d_nrows + nb_el + 1;
-    uint8_t* d_order = (uint8_t*)(d_ntiles + nb_el + 1);
+    int32_t* d_tbase = d_ntiles + nb_el + 1;
+    uint8_t* d_order = (uint8_t*)(d_tbase + nb_el + 1);
     BM_CHECK_CUDA(cudaMemcpyAsync(d_tp_off, tp_off.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_offs, offs.data(), (nb_el + 1) * 8, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_pbase, pbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_nrows, nrows.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_ntiles, ntiles.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_order, order.data(), nb_el, cudaMemcpyHostToDevice, stream));
-    et = ElemTables{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, nb_el};
+    BM_TRY(scratch_alloc(perm, (size_t)(P + n_entries) * 4, stream));
+    ent = perm.as<int32_t>();
+    inv = ent + P;
+    et = ElemTables{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, ent, nb_el};
+    const int64_t* rows_b = d_rows + h_offsets[k0];
+    const bool prune = prune_enabled(d);
 
-    // gather rows (fp64, membership order, padded)
+    // ---- row order inside each element: grouped (stable by seed) or identity
+    {
+      Scratch s_k, s_v, s_it;
+      BM_TRY(scratch_alloc(s_k, (size_t)n_entries * 8, stream));
+      BM_TRY(scratch_alloc(s_v, (size_t)n_entries * 8, stream));
+      std::vector<GroupItem> items;
+      bool any_small = false;
+      const int64_t min_rows = prune ? kGroupMinRows : (1ll << 62);
+      for (int64_t i = 0; i < nb_el; ++i) {
+        if (nrows[i] >= min_rows) {
+          for (int64_t e = offs[i]; e < offs[i + 1]; e += 256)
+            items.push_back({(int32_t)i, (int32_t)e, (int32_t)std::min<int64_t>(e + 256, offs[i + 1]), 0});
+        } else if (nrows[i] > 0) {
+          any_small = true;
+        }
+      }
+      if (any_small) {
+        group_identity_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(
+            d_offs, nb_el, n_entries, min_rows, s_k.as<uint64_t>(), s_v.as<int64_t>());
+        BM_CHECK_LAUNCH();
+      }
+      if (!items.empty()) {
+        BM_TRY(scratch_alloc(s_it, items.size() * sizeof(GroupItem), stream));
+        BM_CHECK_CUDA(cudaMemcpyAsync(s_it.ptr, items.data(), items.size() * sizeof(GroupItem),
+                                      cudaMemcpyHostToDevice, stream));
+        group_assign_kernel<<<(unsigned)items.size(), 128, 0, stream>>>(
+            d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_k.as<uint64_t>(), s_v.as<int64_t>());
+        BM_CHECK_LAUNCH();
+        int bits = 7;
+        while (bits < 64 && ((uint64_t)nb_el << 7) >> bits) ++bits;
+        BM_TRY(sort_pairs_u64(s_k.as<uint64_t>(), s_v.as<int64_t>(), n_entries, bits, stream));
+      }
+      perm_kernel<<<grid_for(P, 256), 256, 0, stream>>>(s_v.as<int64_t>(), d_offs, et, P, ent,
+                                                        inv);
+      BM_CHECK_LAUNCH();
+    }
+
+    // ---- gather rows (fp64, padded order)
     BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
-    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, d_rows + h_offsets[k0], d_offs,
-                                                          et, P, xg.as<double>());
+    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
+                                                          xg.as<double>());
     BM_CHECK_LAUNCH();
 
-    // per-row work arrays (counts accumulate over the adjacency windows)
+    // ---- per-row work arrays (counts accumulate over the adjacency windows)
     const size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
     BM_TRY(scratch_alloc(work, wbytes, stream));
     cnt = work.as<int32_t>();
@@ -637,81 +996,159 @@ struct BatchCtx {
     BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
     if (use_tc) BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc));
+
+    // ---- kept tile pairs and work units (device-built)
+    BM_TRY(build_tiles(d_tbase, prune));
+    stats[3] += n_tp;
+    stats[2] += n_tp - n_kept;
     return BM_OK;
   }
 
-  // Tables addressing the bitmap of tile rows [I0, I1) of element 0 (I0 < 0:
-  // the whole batch). s keeps the shifted tp_off alive.
-  int window(int32_t I0, int32_t I1, ElemTables& etw, int64_t& n_tp_w, Scratch& s) {
-    if (I0 < 0) {
-      etw = et;
-      n_tp_w = n_tp;
-      return BM_OK;
-    }
-    BM_REQUIRE(nb_el == 1 && I0 < I1 && I1 <= ntiles[0], "bad row window [%d, %d)", I0, I1);
-    const int64_t T = ntiles[0];
-    auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
-    const int64_t h[2] = {-tri(I0), -tri(I0) + T * (T + 1) / 2};
-    BM_TRY(scratch_alloc(s, 16, stream));
-    BM_CHECK_CUDA(cudaMemcpyAsync(s.ptr, h, 16, cudaMemcpyHostToDevice, stream));
-    etw = et;
-    etw.tp_off = s.as<int64_t>();
-    n_tp_w = tri(I1) - tri(I0);
-    return BM_OK;
-  }
-
-  // row-tile units of the window: diagonal tiles, then off-diagonal ranges
-  // of <= 32 tiles
-  int units(int32_t I0, int32_t I1, Scratch& s, int64_t& n_diag, int64_t& n_off) {
-    std::vector<TileUnit> hunits;
+  int build_tiles(const int32_t* d_tbase, bool prune) {
+    std::vector<int32_t> row_elem(n_rt);
+    std::vector<PruneBlock> blocks;
     for (int64_t i = 0; i < nb_el; ++i) {
-      const int32_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? ntiles[i] : I1;
-      for (int32_t I = lo; I < hi; ++I) hunits.push_back({(int32_t)i, I, I, I + 1});
+      for (int32_t t = 0; t < ntiles[i]; ++t) row_elem[tbase[i] + t] = (int32_t)i;
+      const int32_t nbk = (int32_t)ceil_div(ntiles[i], kPruneB);
+      for (int32_t bi = 0; bi < nbk; ++bi)
+        for (int32_t bj = bi; bj < nbk; ++bj) blocks.push_back({(int32_t)i, bi, bj, 0});
     }
-    n_diag = (int64_t)hunits.size();
-    for (int64_t i = 0; i < nb_el; ++i) {
-      const int32_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? ntiles[i] : I1;
-      for (int32_t I = lo; I < hi; ++I)
-        for (int32_t J0 = I + 1; J0 < ntiles[i]; J0 += 32)
-          hunits.push_back({(int32_t)i, I, J0, std::min<int32_t>(J0 + 32, ntiles[i])});
-    }
-    n_off = (int64_t)hunits.size() - n_diag;
-    BM_TRY(scratch_alloc(s, std::max<size_t>(1, hunits.size()) * sizeof(TileUnit), stream));
-    if (!hunits.empty())
-      BM_CHECK_CUDA(cudaMemcpyAsync(s.ptr, hunits.data(), hunits.size() * sizeof(TileUnit),
+    Scratch s_re, s_fl, s_pos, s_rows;
+    BM_TRY(scratch_alloc(s_re, n_rt * 4, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(s_re.ptr, row_elem.data(), n_rt * 4, cudaMemcpyHostToDevice, stream));
+    BM_TRY(scratch_alloc(s_fl, (size_t)n_tp * 4, stream));
+    int32_t* flags = s_fl.as<int32_t>();
+    if (prune) {
+      Scratch s_geo, s_blk;
+      BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
+      double* cen = s_geo.as<double>();
+      double* rad = cen + n_rt * d;
+      tile_geom_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(xg.as<double>(), d, et,
+                                                           s_re.as<int32_t>(), cen, rad);
+      BM_CHECK_LAUNCH();
+      const int64_t nblk = (int64_t)blocks.size();
+      BM_TRY(scratch_alloc(s_blk, (size_t)nblk * sizeof(PruneBlock), stream));
+      BM_CHECK_CUDA(cudaMemcpyAsync(s_blk.ptr, blocks.data(), nblk * sizeof(PruneBlock),
                                     cudaMemcpyHostToDevice, stream));
+      const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
+      for (int64_t b0 = 0; b0 < nblk; b0 += (1ll << 30)) {
+        const int64_t nb = std::min<int64_t>(1ll << 30, nblk - b0);
+        tile_prune_kernel<<<(unsigned)nb, 256, 0, stream>>>(et, d, d_tbase,
+                                                            s_blk.as<PruneBlock>() + b0, cen, rad,
+                                                            eps, gamma, flags);
+        BM_CHECK_LAUNCH();
+      }
+    } else {
+      fill_ones_kernel<<<grid_for(n_tp, 256), 256, 0, stream>>>(flags, n_tp);
+      BM_CHECK_LAUNCH();
+    }
+    BM_TRY(scratch_alloc(s_pos, (size_t)(n_tp + 1) * 8, stream));
+    int64_t* pos = s_pos.as<int64_t>();
+    BM_TRY(exclusive_scan_i32_to_i64(flags, pos, n_tp, stream));
+    fill_total_kernel<<<1, 1, 0, stream>>>(pos, flags, n_tp);  // pos[n_tp] = n_kept
+    BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaMemcpyAsync(&n_kept, pos + n_tp, 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    BM_REQUIRE(n_kept < (1ll << 31), "too many tile pairs (%lld)", (long long)n_kept);
+    BM_TRY(scratch_alloc(s_tiles, (size_t)std::max<int64_t>(n_kept, 1) * sizeof(TileRef), stream));
+    d_tiles = s_tiles.as<TileRef>();
+    // row tables: first slot, pairs, unit positions (exclusive scans)
+    BM_TRY(scratch_alloc(s_rows, (size_t)(n_rt + 1) * 8 * 6, stream));
+    int64_t* d_first = s_rows.as<int64_t>();
+    int64_t* d_pairs = d_first + (n_rt + 1);
+    int64_t* d_noff = d_pairs + (n_rt + 1);
+    int64_t* d_ntc = d_noff + (n_rt + 1);
+    int64_t* d_offp = d_ntc + (n_rt + 1);
+    int64_t* d_tcp = d_offp + (n_rt + 1);
+    emit_tiles_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(
+        et, s_re.as<int32_t>(), d_tbase, n_rt, flags, pos, d_tiles, d_first, d_pairs);
+    BM_CHECK_LAUNCH();
+    BM_CHECK_CUDA(cudaMemcpyAsync(d_first + n_rt, pos + n_tp, 8, cudaMemcpyDeviceToDevice, stream));
+    unit_counts_kernel<<<grid_for(n_rt, 256), 256, 0, stream>>>(d_first, n_rt, d_noff, d_ntc);
+    BM_CHECK_LAUNCH();
+    // exclusive scans over n_rt + 1 entries: entry n_rt of the output is the
+    // total (input entry n_rt is never read into it)
+    BM_TRY(exclusive_scan_i64(d_noff, d_offp, n_rt + 1, stream));
+    BM_TRY(exclusive_scan_i64(d_ntc, d_tcp, n_rt + 1, stream));
+    row_first.resize(n_rt + 1);
+    row_pairs.resize(n_rt + 1);
+    off_pos.resize(n_rt + 1);
+    tc_pos.resize(n_rt + 1);
+    BM_CHECK_CUDA(cudaMemcpyAsync(row_first.data(), d_first, (n_rt + 1) * 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(row_pairs.data(), d_pairs, n_rt * 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(off_pos.data(), d_offp, (n_rt + 1) * 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaMemcpyAsync(tc_pos.data(), d_tcp, (n_rt + 1) * 8, cudaMemcpyDeviceToHost, stream));
+    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    const int64_t n_off_u = off_pos[n_rt], n_tc_u = tc_pos[n_rt];
+    BM_TRY(scratch_alloc(s_units, (size_t)(n_rt + n_off_u + n_tc_u + 1) * sizeof(TileUnit), stream));
+    d_diag = s_units.as<TileUnit>();
+    d_off = d_diag + n_rt;
+    d_tcu = d_off + n_off_u;
+    emit_units_kernel<<<grid_for(n_rt, 256), 256, 0, stream>>>(
+        s_re.as<int32_t>(), d_tbase, n_rt, d_first, d_offp, d_tcp, d_diag, d_off, d_tcu);
+    BM_CHECK_LAUNCH();
+    return BM_OK;
+  }
+
+  // kept slots [s0, s1) and row tiles [r0, r1) of the tile rows [I0, I1) of
+  // element 0 (I0 < 0: the whole batch)
+  void rows_of(int32_t I0, int32_t I1, int64_t& r0, int64_t& r1) const {
+    if (I0 < 0) {
+      r0 = 0;
+      r1 = n_rt;
+    } else {
+      r0 = tbase[0] + I0;
+      r1 = tbase[0] + I1;
+    }
+  }
+
+  // device views of the window's tiles and work units (no copies: the
+  // window is a contiguous run of rows, hence of slots and of every unit list)
+  int window(int32_t I0, int32_t I1, WindowBufs& w) {
+    if (I0 >= 0)
+      BM_REQUIRE(nb_el == 1 && I0 < I1 && I1 <= ntiles[0], "bad row window [%d, %d)", I0, I1);
+    int64_t r0 = 0, r1 = 0;
+    rows_of(I0, I1, r0, r1);
+    w.slot0 = row_first[r0];
+    w.n_tiles = row_first[r1] - row_first[r0];
+    w.tiles = d_tiles;
+    w.diag = d_diag + r0;
+    w.n_diag = r1 - r0;
+    w.off = d_off + off_pos[r0];
+    w.n_off = off_pos[r1] - off_pos[r0];
+    w.tcu = d_tcu + tc_pos[r0];
+    w.n_tc = tc_pos[r1] - tc_pos[r0];
+    w.pairs = 0;
+    for (int64_t r = r0; r < r1; ++r) w.pairs += row_pairs[r];
     return BM_OK;
   }
 
   // Bits of the window into adj; counts added into cnt_acc (nullptr: the
   // counts of this window were already taken).
   int adjacency(int32_t I0, int32_t I1, uint32_t* adj, int32_t* cnt_acc, int64_t* stats) {
-    ElemTables etw;
-    int64_t n_tp_w = 0;
-    Scratch s_w;
-    BM_TRY(window(I0, I1, etw, n_tp_w, s_w));
+    WindowBufs w;
+    BM_TRY(window(I0, I1, w));
     if (use_tc) {
-      BM_TRY(tc_window(tc, xg.as<double>(), etw, n_tp_w, I0, I1, adj, cnt_acc, I0 >= 0, stats,
-                       stream));
+      BM_TRY(tc_window(tc, xg.as<double>(), et, w.tiles, w.slot0, w.n_tiles, w.tcu, w.n_tc,
+                       w.pairs, adj, cnt_acc, I0 >= 0, stats, stream));
     } else {
-      BM_TRY(exact_build_adjacency(xg.as<double>(), d, etw, n_tp_w, eps, adj, stream));
+      BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, w.tiles + w.slot0, w.n_tiles, eps,
+                                   adj, stream));
       if (cnt_acc) {
-        Scratch s_u;
-        int64_t n_diag = 0, n_off = 0;
-        BM_TRY(units(I0, I1, s_u, n_diag, n_off));
-        count_kernel<<<grid_for(n_diag + n_off, 1, 32), 128, 0, stream>>>(
-            adj, etw, s_u.as<TileUnit>(), n_diag + n_off, cnt_acc);
-        BM_CHECK_LAUNCH();
+        if (w.n_diag > 0) {
+          count_kernel<<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
+              adj, et, w.diag, w.tiles, w.slot0, w.n_diag, cnt_acc);
+          BM_CHECK_LAUNCH();
+        }
+        if (w.n_off > 0) {
+          count_kernel<<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
+              adj, et, w.off, w.tiles, w.slot0, w.n_off, cnt_acc);
+          BM_CHECK_LAUNCH();
+        }
       }
-      for (int64_t i = 0; i < nb_el; ++i) {
-        const int64_t nk = nrows[i];
-        const int64_t lo = I0 < 0 ? 0 : (int64_t)I0 * kTile;
-        const int64_t hi = I0 < 0 ? nk : std::min<int64_t>((int64_t)I1 * kTile, nk);
-        for (int64_t r = lo; r < hi; ++r) stats[0] += nk - 1 - r;  // distinct pairs (r, >r)
-      }
+      stats[0] += w.pairs;
     }
-    stats[3] += n_tp_w;
-    stats[4] = std::max<int64_t>(stats[4], n_tp_w * kTileWords * 4);
+    stats[4] = std::max<int64_t>(stats[4], w.n_tiles * kTileWords * 4);
     return BM_OK;
   }
 
@@ -724,42 +1161,46 @@ struct BatchCtx {
 
   // union-find over the core-core bits and border minima of the window
   int components(int32_t I0, int32_t I1, const uint32_t* adj, int32_t* par_w, int32_t* bmin_w) {
-    ElemTables etw;
-    int64_t n_tp_w = 0;
-    Scratch s_w, s_u;
-    BM_TRY(window(I0, I1, etw, n_tp_w, s_w));
-    int64_t n_diag = 0, n_off = 0;
-    BM_TRY(units(I0, I1, s_u, n_diag, n_off));
-    const TileUnit* d_diag = s_u.as<TileUnit>();
-    components_kernel<true><<<grid_for(n_diag, 1, 32), 128, 0, stream>>>(adj, etw, d_diag, n_diag,
-                                                                         core, par_w, bmin_w);
-    BM_CHECK_LAUNCH();
+    WindowBufs w;
+    BM_TRY(window(I0, I1, w));
+    if (w.n_diag > 0) {
+      components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
+          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w);
+      BM_CHECK_LAUNCH();
+    }
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
     BM_CHECK_LAUNCH();
-    if (n_off > 0) {
-      components_kernel<false><<<grid_for(n_off, 1, 32), 128, 0, stream>>>(
-          adj, etw, d_diag + n_diag, n_off, core, par_w, bmin_w);
+    if (w.n_off > 0) {
+      components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
+          adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w);
       BM_CHECK_LAUNCH();
     }
     return BM_OK;
   }
 
+  // bytes of the bitmap of the row tiles [I0, I1) (all: I0 < 0)
+  size_t window_bytes(int32_t I0, int32_t I1) const {
+    int64_t r0 = 0, r1 = 0;
+    rows_of(I0, I1, r0, r1);
+    return (size_t)std::max<int64_t>(row_first[r1] - row_first[r0], 1) * kTileWords * 4;
+  }
+
   // canonical labels of every entry (element-relative cluster ids, -1 noise)
   int finish(int32_t* par_w, const int32_t* bmin_w, int32_t* d_out, int32_t* h_ncl) {
-    label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par_w, bmin_w, lab, cmin);
+    label_kernel<<<grid_for(P, 256), 256, 0, stream>>>(et, P, core, par_w, bmin_w, inv, lab, cmin);
     BM_CHECK_LAUNCH();
-    head_kernel<<<grid_for(P, 256), 256, 0, stream>>>(P, lab, cmin, head);
+    head_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(n_entries, inv, lab, cmin, head);
     BM_CHECK_LAUNCH();
-    BM_TRY(exclusive_scan_i32_to_i64(head, hscan, P, stream));
-    fill_total_kernel<<<1, 1, 0, stream>>>(hscan, head, P);  // hscan[P] = #heads
+    BM_TRY(exclusive_scan_i32_to_i64(head, hscan, n_entries, stream));
+    fill_total_kernel<<<1, 1, 0, stream>>>(hscan, head, n_entries);  // hscan[n] = #heads
     BM_CHECK_LAUNCH();
     Scratch ncl_d;
     BM_TRY(scratch_alloc(ncl_d, nb_el * 4, stream));
-    nclusters_kernel<<<(unsigned)ceil_div(nb_el, 128), 128, 0, stream>>>(et, hscan,
+    nclusters_kernel<<<(unsigned)ceil_div(nb_el, 128), 128, 0, stream>>>(et, d_offs, hscan,
                                                                           ncl_d.as<int32_t>());
     BM_CHECK_LAUNCH();
-    output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(et, d_offs, n_entries, lab, cmin,
-                                                                hscan, d_out);
+    output_kernel<<<grid_for(n_entries, 256), 256, 0, stream>>>(et, d_offs, n_entries, inv, lab,
+                                                                cmin, hscan, d_out);
     BM_CHECK_LAUNCH();
     BM_CHECK_CUDA(cudaMemcpyAsync(h_ncl, ncl_d.ptr, nb_el * 4, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
@@ -767,17 +1208,20 @@ struct BatchCtx {
   }
 };
 
-// Row windows of a T-tile triangle holding at most max_tiles tile pairs each
-// (every window has at least one tile row), in ascending row order. Built
-// from the bottom so that the LAST window — the one whose bits stay resident
-// between the two passes — is the full one and the recomputed remainder is
-// as small as possible.
-std::vector<std::pair<int32_t, int32_t>> row_windows(int64_t T, int64_t max_tiles) {
+// Row windows of element 0 holding at most max_tiles kept tiles each (every
+// window has at least one tile row), in ascending row order. Built from the
+// bottom so that the LAST window — the one whose bits stay resident between
+// the two passes — is the full one and the recomputed remainder is as small
+// as possible.
+std::vector<std::pair<int32_t, int32_t>> row_windows(const BatchCtx& bc, int64_t max_tiles) {
+  const int64_t T = bc.ntiles[0];
+  auto first = [&](int64_t I) { return bc.row_first[bc.tbase[0] + I]; };
+  // first(I) = slot of row I's diagonal; rows [I, I1) hold first(I1) - first(I) tiles
   std::vector<std::pair<int32_t, int32_t>> w;
   int64_t I1 = T;
   while (I1 > 0) {
-    int64_t acc = 0, I = I1;
-    while (I > 0 && (I == I1 || acc + (T - (I - 1)) <= max_tiles)) acc += T - --I;
+    int64_t I = I1 - 1;
+    while (I > 0 && first(I1) - first(I - 1) <= max_tiles) --I;
     w.push_back({(int32_t)I, (int32_t)I1});
     I1 = I;
   }
@@ -790,6 +1234,9 @@ int64_t row_window_cap() {
   const char* e = getenv("B200MAP_WINDOW_TILES");
   return e ? std::max<int64_t>(1, atoll(e)) : 0;
 }
+
+// bytes per kept tile besides its bitmap: tile ref, thresholds, recheck queue
+constexpr double kTileAux = 16.0 + 24.0 + 16.0 * 16384.0 / 2000.0;
 
 }  // namespace bm
 
@@ -819,6 +1266,7 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
   }
   if (h_offsets[n_el] == h_offsets[0]) return BM_OK;
   BM_REQUIRE(d_X && d_rows && d_labels, "null device pointer");
+  BM_REQUIRE(h_offsets[n_el] - h_offsets[0] < (1ll << 31), "too many membership entries");
   PwProgram probe;
   BM_TRY(make_pw_program(d, &probe));
 
@@ -830,15 +1278,16 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     use_tc = tc_supported(d);
   }
 
-  // ---- batches bounded by the device budget; an element whose bitmap alone
-  //      exceeds it is processed by itself in row windows
+  // ---- batches bounded by the device budget (dense bitmap estimate); an
+  //      element whose dense bitmap alone exceeds it is processed by itself in
+  //      row windows sized on its kept tiles
   size_t free_b = 0;
   BM_TRY(device_free_bytes(&free_b));
   const double budget = 0.55 * (double)free_b;
   const int64_t forced_cap = row_window_cap();
   struct Batch {
     int64_t k0, k1;
-    int64_t window_tiles;  // > 0: single huge element in row windows
+    bool windowed;  // single huge element in row windows
   };
   std::vector<Batch> batches;
   {
@@ -848,33 +1297,23 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       const int64_t nk = h_offsets[k + 1] - h_offsets[k];
       const int64_t T = ceil_div(nk, kTile);
       BM_REQUIRE(T * kTile < (1ll << 31), "element %lld too large", (long long)k);
-      const double row_bytes = (double)T * kTile * (d * 8.0 + 4 * 7 + 1 + 8 + d * 3.0);
-      const double bytes = (double)(T * (T + 1) / 2) * kTileWords * 4 + row_bytes;
+      const double row_bytes = (double)T * kTile * (d * 8.0 + 4 * 9 + 1 + 24 + d * 3.0);
+      const double bytes = (double)(T * (T + 1) / 2) * (kTileWords * 4 + kTileAux) + row_bytes;
       if (bytes > budget || (forced_cap > 0 && T * (T + 1) / 2 > forced_cap)) {
-        if (k > k0) batches.push_back({k0, k, 0});
-        // the window may use most of the free memory: besides the rows it
-        // needs ~8 B per tile pair for thresholds and the recheck queue
-        const double win_bytes = 0.85 * (double)free_b - row_bytes - (4ll << 30);
-        int64_t cap = (int64_t)(win_bytes / (kTileWords * 4.0 + 8.0));
-        if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
-        else if (cap < T) {
-          set_error("element %lld (%lld rows) leaves no room for one row window of its "
-                    "eps-graph (budget %.1f GB)", (long long)k, (long long)nk, budget / 1e9);
-          return BM_ERR_NOMEM;
-        }
-        batches.push_back({k, k + 1, cap});
+        if (k > k0) batches.push_back({k0, k, false});
+        batches.push_back({k, k + 1, true});
         k0 = k + 1;
         acc = 0;
         continue;
       }
       if (acc + bytes > budget && k > k0) {
-        batches.push_back({k0, k, 0});
+        batches.push_back({k0, k, false});
         k0 = k;
         acc = 0;
       }
       acc += bytes;
     }
-    if (k0 < n_el) batches.push_back({k0, n_el, 0});
+    if (k0 < n_el) batches.push_back({k0, n_el, false});
   }
 
   for (const Batch& bt : batches) {
@@ -896,52 +1335,46 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     bc.eps = eps;
     bc.min_pts = min_pts;
     bc.use_tc = use_tc;
-    BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1));
+    BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1, stats));
     if (bc.n_entries == 0) continue;
     int32_t* d_out = d_labels + h_offsets[bt.k0];
     float ms = 0.f, ms_pre = 0.f, ms_post = 0.f;
-    if (bt.window_tiles == 0) {
-      Scratch adj;
-      BM_TRY(scratch_alloc(adj, (size_t)bc.n_tp * kTileWords * 4, stream));
-      BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
-      BM_TRY(bc.adjacency(-1, -1, adj.as<uint32_t>(), bc.cnt, stats));
-      BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
-      BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
-      BM_TRY(bc.components(-1, -1, adj.as<uint32_t>(), bc.par, bc.bmin));
-      BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
-      BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
+    std::vector<std::pair<int32_t, int32_t>> wins;
+    if (bt.windowed) {
+      size_t free_now = 0;
+      BM_TRY(device_free_bytes(&free_now));
+      int64_t cap = (int64_t)((0.85 * (double)free_now - (double)(2ll << 30)) /
+                              (kTileWords * 4.0 + kTileAux));
+      if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
+      wins = row_windows(bc, std::max<int64_t>(cap, 1));
     } else {
-      // pass 1: counts of every window (the last window's bits stay resident);
-      // pass 2: components of the resident window, then of the others with
-      // their bits recomputed (bit-identical: the decision is a pure function
-      // of the pair)
-      const auto wins = row_windows(bc.ntiles[0], bt.window_tiles);
-      int64_t max_w = 0;
-      for (auto& w : wins) {
-        const int64_t T = bc.ntiles[0];
-        auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
-        max_w = std::max<int64_t>(max_w, tri(w.second) - tri(w.first));
-      }
-      Scratch adj;
-      BM_TRY(scratch_alloc(adj, (size_t)max_w * kTileWords * 4, stream));
-      BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
-      for (auto& w : wins) BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, stats));
-      BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
-      BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
-      for (size_t i = wins.size(); i-- > 0;) {
-        if (i + 1 != wins.size())
-          BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, stats));
-        BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
-      }
-      BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
-      BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
+      wins.push_back({-1, -1});
     }
+    size_t max_w = 0;
+    for (auto& w : wins) max_w = std::max(max_w, bc.window_bytes(w.first, w.second));
+    Scratch adj;
+    BM_TRY(scratch_alloc(adj, max_w, stream));
+    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+    // pass 1: counts of every window (the last window's bits stay resident);
+    // pass 2: components of the resident window, then of the others with
+    // their bits recomputed (bit-identical: the decision is a pure function of
+    // the pair)
+    for (auto& w : wins) BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, stats));
+    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+    BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
+    for (size_t i = wins.size(); i-- > 0;) {
+      if (i + 1 != wins.size())
+        BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, stats));
+      BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
+    }
+    BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
+    BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
     BM_CHECK_CUDA(cudaEventSynchronize(ev2));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms_pre, evs, ev0));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms_post, ev1, ev2));
     stats[5] += (int64_t)(ms * 1e6);       // adjacency (distance) stage, ns on the launch stream
-    stats[6] += (int64_t)(ms_pre * 1e6);   // gather + setup (+ quantisation)
+    stats[6] += (int64_t)(ms_pre * 1e6);   // grouping, gather, quantisation, pruning
     stats[7] += (int64_t)(ms_post * 1e6);  // core, union-find, border, relabel (+ recomputed windows)
   }
   return BM_OK;
@@ -967,11 +1400,8 @@ struct BigElement {
 
   int bits(int32_t I0, int32_t I1, int32_t* cnt_acc) {
     BM_REQUIRE(I0 >= 0 && I0 < I1 && I1 <= bc.ntiles[0], "bad row window [%d, %d)", I0, I1);
-    const int64_t T = bc.ntiles[0];
-    auto tri = [T](int64_t I) { return I * T - I * (I - 1) / 2; };
-    const size_t need = (size_t)(tri(I1) - tri(I0)) * kTileWords * 4;
+    const size_t need = bc.window_bytes(I0, I1);
     if (need > adj_bytes) {
-      adj.release();
       BM_TRY(scratch_alloc(adj, need, bc.stream));
       adj_bytes = need;
     }
@@ -1021,7 +1451,7 @@ extern "C" int bm_big_open(const double* d_X, int64_t n, int64_t d, const int64_
   be->bc.use_tc = use_tc;
   const int64_t offs[2] = {0, n_rows};
   const uint8_t ord = (uint8_t)order;
-  const int rc = be->bc.setup(d_X, d_rows, offs, &ord, 0, 1);
+  const int rc = be->bc.setup(d_X, d_rows, offs, &ord, 0, 1, be->stats);
   if (rc != BM_OK) {
     delete be;
     return rc;

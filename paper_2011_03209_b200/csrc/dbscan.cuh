@@ -1,16 +1,22 @@
 // dbscan.cuh — shared layout of the per-element DBSCAN engine.
 //
 // Layout in HBM (one batch of elements):
-//   padded index p = pbase[k] + i  (i = position of the row inside element k;
-//                    pbase rounds every element up to a multiple of kTile)
-//   Xg   : P x d fp64   rows gathered in membership order (pads are zero)
-//   adj  : triangular tile pairs (I <= J) of every element, each a 128x128
-//          bit tile stored as 128 rows x 4 uint32 words (2 KiB); tile pair
-//          (I, J) of element k lives at tile index tp_off[k] + tri(I, J, T_k)
+//   entry e   = position of a membership entry in the batch (element-major,
+//               ascending rows inside an element: the reference's order)
+//   padded index p = pbase[k] + i: element k's rows in a SPATIALLY GROUPED
+//               order (nearest-seed groups, stable), padded to kTile rows;
+//               ent[p] = e (-1 for pads), inv[e] = p. Every order-dependent
+//               rule of the reference (border -> smallest core neighbour,
+//               clusters ordered by smallest member) is evaluated on e.
+//   Xg   : P x d fp64   rows gathered in padded order (pads are zero)
+//   tiles: the KEPT tile pairs (I <= J) of every element, sorted by (k, I, J):
+//          pairs whose rigorous centroid/radius bound puts every row pair
+//          beyond eps are pruned (they hold no bit). Slot s of the list owns
+//          the 128x128 bit tile adj[s] (128 rows x 4 uint32 words, 2 KiB).
 //   cnt  : int32 per p   eps-neighbour counts (self included)
 //   core : uint8 per p
 //   par  : int32 per p   union-find parent (root = min padded index)
-//   bmin : int32 per p   smallest core neighbour of a non-core point
+//   bmin : int32 per p   smallest-ENTRY core neighbour of a non-core point
 #pragma once
 #include "common.cuh"
 
@@ -21,17 +27,24 @@ constexpr int kTileWords = kTile * kTile / 32;  // 512
 constexpr int kNoCore = 0x7fffffff;
 
 struct ElemTables {
-  const int64_t* tp_off;  // n_el+1 tile-pair prefix
+  const int64_t* tp_off;  // n_el+1 dense tile-pair prefix (pruning flags)
   const int32_t* pbase;   // n_el+1 padded base
   const int32_t* nrows;   // n_el
   const int32_t* ntiles;  // n_el
   const uint8_t* order;   // n_el (BM_ORDER_*)
+  const int32_t* ent;     // P: batch entry of padded row p (-1: pad)
   int64_t n_el;
 };
 
-// row-tile work unit: element k, row tile I, column tiles [J0, J1)
+// kept tile pair: element k, row tile I, column tile J (slot = list index)
+struct TileRef {
+  int32_t k, I, J, pad;
+};
+
+// row-tile work unit: element k, row tile I, slots [off, off + cnt) of the
+// window's kept-tile list (all with row tile I, ascending J)
 struct TileUnit {
-  int32_t k, I, J0, J1;
+  int32_t k, I, off, cnt;
 };
 
 __device__ __forceinline__ int64_t tri_index(int64_t I, int64_t J, int64_t T) {

@@ -296,6 +296,11 @@ inline unsigned grid1(int64_t n, int threads = 256) {
 }
 
 }  // namespace
+
+int sort_pairs_u64(uint64_t* keys, int64_t* vals, int64_t n, int key_bits, cudaStream_t s) {
+  return radix_sort_pairs(keys, vals, n, key_bits, s);
+}
+
 }  // namespace bm
 
 using namespace bm;

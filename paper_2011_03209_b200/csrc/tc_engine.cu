@@ -43,9 +43,6 @@
 
 namespace bm {
 
-int exact_adjacency_for(const double* Xg, int64_t d, const ElemTables& et, int64_t n_tp,
-                        double eps, uint32_t* adj, cudaStream_t stream);
-
 namespace {
 
 constexpr int kBM = 128;        // A rows (TMEM lanes)
@@ -60,10 +57,6 @@ constexpr int kThreads = 128 + 32 * (kEpiWarps + kLoadWarps);
 constexpr int kLimb = 7;        // bits of the M and L limbs
 constexpr int kQBits = 2 * kLimb + 7;   // |q| <= 2^21 - 1: H = q >> 14 is a signed byte
 constexpr int kYShift = 3 * kLimb + 1;  // y is in units of 2^22 of D2
-
-struct Unit {
-  int32_t k, I, b0, b1;
-};
 
 __constant__ PwProgram c_prog_tc;
 
@@ -189,8 +182,10 @@ constexpr int kYMax = 850000000;  // bound on |y| (kLimb = 7, Kpad <= 256): see 
 
 struct TcParams {
   ElemTables et;
-  const TileThr* thr;     // per bitmap tile pair
-  const Unit* units;
+  const TileThr* thr;     // per kept tile (slot)
+  const TileRef* tiles;   // kept tiles of the batch (absolute slot -> k, I, J)
+  int64_t slot0;          // first slot of the window (adj, thr, queue use slot - slot0)
+  const TileUnit* units;
   int64_t n_units;
   const int64_t* nq;      // per padded row: sum q^2
   const int32_t* cq;      // per padded row: floor(sum q^2 / 2^kYShift)
@@ -203,7 +198,7 @@ struct TcParams {
   int nkc;                // Kpad / 128
   uint32_t* adj;
   int32_t* cnt;           // eps-neighbour counts per padded row (self included)
-  int2* queue;
+  int4* queue;            // undecided pairs: (p_i, p_j, slot, element)
   const uint8_t* planes;  // limb planes [3][P][kpad]
   int64_t P;
   unsigned long long* qcount;
@@ -234,11 +229,11 @@ __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI,
 // niU = floor(N_i/U),
 //   r_in  = niU + ceil(-t_in/U) + 3   >= (N_i - t_in)/U + 2
 //   r_out = niU + floor(-(t_out + a3max)/U) - 2 <= (N_i - t_out - a3max)/U - 1
-__global__ void tile_thr_kernel(TcParams P, int64_t n_tp, TileThr* __restrict__ out) {
+__global__ void tile_thr_kernel(TcParams P, int64_t n_tiles, TileThr* __restrict__ out) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_tp) return;
-  int k, I, J;
-  decode_tile(P.et, g, k, I, J);
+  if (g >= n_tiles) return;
+  const TileRef tr = P.tiles[P.slot0 + g];
+  const int k = tr.k, I = tr.I, J = tr.J;
   double t_in, t_out;
   thresholds(P, k, P.tbase[k] + I, P.tbase[k] + J, t_in, t_out);
   TileThr th;
@@ -368,11 +363,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       uint32_t stage = 0, ph_empty[kStages] = {0, 0}, a_empty_ph = 0;
       uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
       for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-        const Unit un = P.units[u];
+        const TileUnit un = P.units[u];
         const int pb = P.et.pbase[un.k];
         // A limb plane L of row tile I (resident for the unit)
-        const int64_t tpk = P.et.tp_off[un.k];
-        const int64_t T = P.et.ntiles[un.k];
         mbar_wait(a_empty, a_empty_ph ^ 1);
         a_empty_ph ^= 1;
         mbar_expect_tx(a_sm_full, aL_bytes);
@@ -380,11 +373,12 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           for (int h = 0; h < 2; ++h)
             tma_load_3d(sAL + c * blk + h * 64 * kKC, &qmap, a_sm_full, c * kKC,
                         pb + un.I * kBM + h * 64, 2);
-        for (int b = un.b0; b < un.b1; ++b) {
+        for (int t = 0; t < un.cnt; ++t) {
+          const int b = P.tiles[un.off + t].J;
           // tile info for the epilogue (runs ahead by up to kInfo tiles)
           mbar_wait(info_empty + islot, ph_info[islot] ^ 1);
           ph_info[islot] ^= 1;
-          info[islot].th = *reinterpret_cast<const int2*>(P.thr + tpk + tri_index(un.I, b, T));
+          info[islot].th = *reinterpret_cast<const int2*>(P.thr + (un.off + t - P.slot0));
           mbar_expect_tx(info_full + islot, kBN * 4);
           bulk_load(info[islot].cq, P.cq + pb + b * kBN, kBN * 4, info_full + islot);
           islot = (islot + 1) % kInfo;
@@ -421,14 +415,14 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     long long prof_a = 0, prof_b = 0, prof_e0 = 0, prof_e1 = 0;
     const long long prof_t0 = clock64();
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-      const Unit un = P.units[u];
+      const TileUnit un = P.units[u];
       long long tw = clock64();
       mbar_wait(a_tm_full, a_ph);
       mbar_wait(a_sm_full, a_ph);
       prof_a += clock64() - tw;
       a_ph ^= 1;
       tc_fence_after();
-      for (int b = un.b0; b < un.b1; ++b) {
+      for (int t = 0; t < un.cnt; ++t) {
         tw = clock64();
         mbar_wait(b_full + stage, ph_full[stage]);
         prof_b += clock64() - tw;
@@ -485,7 +479,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     const uint32_t ncol_plane = (uint32_t)kpad / 4;
     uint32_t a_empty_ph = 0;
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-      const Unit un = P.units[u];
+      const TileUnit un = P.units[u];
       const int64_t prow = (int64_t)P.et.pbase[un.k] + un.I * kBM + row;
       mbar_wait(a_empty, a_empty_ph ^ 1);
       a_empty_ph ^= 1;
@@ -513,7 +507,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       // warm L2 with the next unit's A rows
       const int64_t un_next = u + gridDim.x;
       if (un_next < P.n_units) {
-        const Unit nx = P.units[un_next];
+        const TileUnit nx = P.units[un_next];
         const int64_t nrow = (int64_t)P.et.pbase[nx.k] + nx.I * kBM + row;
         for (int pl = 0; pl < 2; ++pl)
           for (int off = 0; off < kpad; off += 128)
@@ -536,19 +530,18 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     const long long ep_t0 = clock64();
 #endif
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-      const Unit un = P.units[u];
+      const TileUnit un = P.units[u];
       const int k = un.k;
       const int pb = P.et.pbase[k];
       const int n_k = P.et.nrows[k];
-      const int64_t T = P.et.ntiles[k];
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
       const int niU = (int)(P.nq[pb + gi] >> kYShift);
       int row_count = 0;
-      const int64_t tpk = P.et.tp_off[k];
-      for (int J = un.b0; J < un.b1; ++J) {
+      for (int t = 0; t < un.cnt; ++t) {
+        const int J = P.tiles[un.off + t].J;
+        const int64_t tile = un.off + t - P.slot0;    // window slot of the kept tile
         const int col0 = J * kBN + ch * 64;           // first local column of this warp
-        const int64_t tile = tpk + tri_index(un.I, J, T);
         // Integer decision. With y = 2^7 a0 + a1 + (a2 >> 7) - floor(N_j/U):
         //   y >= r_in  => D2c <= t_in (certainly inside; a3, L.L >= 0)
         //   y <= r_out => D2c >  t_out (certainly outside; a3, L.L bounded)
@@ -687,7 +680,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
               while (band) {
                 const int j = __ffs(band) - 1;
                 band &= band - 1;
-                if (i < P.qcap) P.queue[i] = make_int2(pb + gi, pb + col0 + h * 32 + j);
+                if (i < P.qcap)
+                  P.queue[i] = make_int4(pb + gi, pb + col0 + h * 32 + j, (int)tile, k);
                 ++i;
               }
             }
@@ -849,12 +843,13 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
   }
 }
 
-__device__ __forceinline__ void set_inside(const ElemTables& et, int k, int2 pr,
+__device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
                                            uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
                                            unsigned long long* __restrict__ n_inside) {
+  const int k = pr.w;
   const int li = pr.x - et.pbase[k], lj = pr.y - et.pbase[k];
   const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
-  const int64_t tile = et.tp_off[k] + tri_index(I, J, et.ntiles[k]);
+  const int64_t tile = pr.z;
   atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
   atomicAdd(cnt + pr.x, 1);
   if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
@@ -874,7 +869,7 @@ constexpr int kRcWarps = 4;
 
 __global__ void __launch_bounds__(kRcWarps * 32)
     recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
-                   const int2* __restrict__ queue, int64_t nq, double eps,
+                   const int4* __restrict__ queue, int64_t nq, double eps,
                    uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
                    unsigned long long* __restrict__ n_inside) {
   __shared__ double sq_all[kRcWarps][32][33];
@@ -885,16 +880,8 @@ __global__ void __launch_bounds__(kRcWarps * 32)
        base += stride) {
     const int64_t i = base + lane;
     const bool have = i < nq;
-    const int2 pr = have ? queue[i] : make_int2(0, 0);
-    int k = 0;
-    if (have) {
-      int64_t a = 0, bb = et.n_el;
-      while (bb - a > 1) {
-        const int64_t mid = (a + bb) >> 1;
-        if (et.pbase[mid] <= pr.x) a = mid; else bb = mid;
-      }
-      k = (int)a;
-    }
+    const int4 pr = have ? queue[i] : make_int4(0, 0, 0, 0);
+    const int k = pr.w;
     const int np = (nq - base) < 32 ? (int)(nq - base) : 32;
     double s_seq = 0.0, res = 0.0;
     double r[8];
@@ -964,7 +951,7 @@ __global__ void __launch_bounds__(kRcWarps * 32)
     }
     if (have) {
       const double s2 = et.order[k] == BM_ORDER_SEQUENTIAL ? s_seq : __dadd_rn(0.0, st.s[0]);
-      if (__dsqrt_rn(s2) <= eps) set_inside(et, k, pr, adj, cnt, n_inside);
+      if (__dsqrt_rn(s2) <= eps) set_inside(et, pr, adj, cnt, n_inside);
     }
   }
 }
@@ -1117,39 +1104,20 @@ __global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __re
     if (src[i]) dst[i] += src[i];
 }
 
-// Adjacency bits and eps-neighbour counts of the tile rows [I0, I1) of every
-// element (I0 < 0: all rows). `et` addresses the bitmap window being written
-// (for a window, tp_off[k] = -tri(I0, I0, T)); n_tp = tiles in that window.
+// Adjacency bits and eps-neighbour counts of one window of kept tiles:
+// slots [slot0, slot0 + n_tiles) of the batch list `tiles`, work units over
+// them; adj[slot - slot0] written.
 // accumulate: add the window's counts into cnt instead of overwriting it;
 // cnt == nullptr: the counts of this window are not wanted (recomputed window).
-int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, int32_t I0,
-              int32_t I1, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
+// pairs = distinct row pairs inside the window's tiles (stats and queue size).
+int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
+              int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
+              int64_t pairs, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
               cudaStream_t stream) {
-  const int64_t n_el = tp->n_el, P = tp->P, d = tp->d;
+  const int64_t P = tp->P, d = tp->d;
   const int nkc = tp->nkc;
-  std::vector<Unit> units;
-  int64_t pairs = 0;
-  for (int64_t k = 0; k < n_el; ++k) {
-    const int64_t T = ceil_div(tp->nrows[k], kTile);
-    const int64_t lo = I0 < 0 ? 0 : I0, hi = I0 < 0 ? T : std::min<int64_t>(I1, T);
-    for (int64_t I = lo; I < hi; ++I) {
-      for (int64_t b0 = I; b0 < T; b0 += kUnitB)
-        units.push_back({(int32_t)k, (int32_t)I, (int32_t)b0,
-                         (int32_t)std::min<int64_t>(b0 + kUnitB, T)});
-      // unordered distinct pairs of this tile row (its rows against every later row)
-      const int64_t r0 = I * kTile, r1 = std::min<int64_t>(r0 + kTile, tp->nrows[k]);
-      if (r1 > r0) {
-        const int64_t m = r1 - r0, rest = tp->nrows[k] - r1;
-        pairs += m * (m - 1) / 2 + m * rest;
-      }
-    }
-  }
-  const int64_t n_units = (int64_t)units.size();
   if (n_units == 0) return BM_OK;
-  Scratch s_units, s_q, s_cnt, s_tt;
-  BM_TRY(scratch_alloc(s_units, n_units * sizeof(Unit), stream));
-  BM_CHECK_CUDA(cudaMemcpyAsync(s_units.ptr, units.data(), n_units * sizeof(Unit),
-                                cudaMemcpyHostToDevice, stream));
+  Scratch s_q, s_cnt, s_tt;
   int32_t* cnt_run = cnt;
   if (accumulate || !cnt) {  // window counts go to a private buffer first
     if (!tp->s_cntw.ptr) BM_TRY(scratch_alloc(tp->s_cntw, (size_t)P * 4, stream));
@@ -1158,7 +1126,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
 
   // ---- MMA pass (re-run with a larger recheck queue on overflow)
   unsigned long long qcap =
-      std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 10000));
+      std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 2000));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
   const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;
@@ -1170,15 +1138,17 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  BM_TRY(scratch_alloc(s_tt, (size_t)n_tp * sizeof(TileThr), stream));
+  BM_TRY(scratch_alloc(s_tt, (size_t)n_tiles * sizeof(TileThr), stream));
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
-    BM_TRY(scratch_alloc(s_q, qcap * sizeof(int2), stream));
+    BM_TRY(scratch_alloc(s_q, qcap * sizeof(int4), stream));
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));
     TcParams prm{};
     prm.et = et;
-    prm.units = s_units.as<Unit>();
+    prm.units = units;
+    prm.tiles = tiles;
+    prm.slot0 = slot0;
     prm.n_units = n_units;
     prm.nq = tp->s_nq.as<int64_t>();
     prm.cq = reinterpret_cast<const int32_t*>(tp->s_nq.as<int64_t>() + P);
@@ -1192,7 +1162,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
     prm.nkc = nkc;
     prm.adj = adj;
     prm.cnt = cnt_run;
-    prm.queue = s_q.as<int2>();
+    prm.queue = s_q.as<int4>();
     prm.planes = tp->s_pl.as<uint8_t>();
     prm.P = P;
     prm.qcount = d_cnt;
@@ -1206,8 +1176,8 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
     }
     prm.thr = s_tt.as<TileThr>();
     if (attempt == 0) {
-      tile_thr_kernel<<<(unsigned)ceil_div(n_tp, 256), 256, 0, stream>>>(prm, n_tp,
-                                                                         s_tt.as<TileThr>());
+      tile_thr_kernel<<<(unsigned)ceil_div(n_tiles, 256), 256, 0, stream>>>(prm, n_tiles,
+                                                                             s_tt.as<TileThr>());
       BM_CHECK_LAUNCH();
     }
     const unsigned grid = (unsigned)std::min<int64_t>(num_sms(), n_units);
@@ -1247,7 +1217,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, int64_t n_tp, 
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
     recheck_kernel<<<grid_cap(nrec, kRcWarps * 32, 8), kRcWarps * 32, 0, stream>>>(
-        Xg, d, et, s_q.as<int2>(), nrec, tp->eps, adj, cnt_run, d_cnt + 1);
+        Xg, d, et, s_q.as<int4>(), nrec, tp->eps, adj, cnt_run, d_cnt + 1);
     BM_CHECK_LAUNCH();
   }
   if (accumulate && cnt) {

@@ -24,4 +24,4 @@ for name in names:
         torch.cuda.synchronize(); el = time.time() - t
         print(f"{name} it{it} engine={engine} total={el:.3f}s stages={ {k: round(v,4) for k,v in g.timings.items()} } "
               f"nodes={g.n_nodes} edges={len(g.edges)} sum_nk={int(g.sizes.sum())} max_nk={int(g.sizes.max())} "
-              f"sum_nk2={float((g.sizes.astype(np.float64)**2).sum()):.3e} adj_ms={g.dev_stats[5]/1e6:.1f} pre_ms={g.dev_stats[6]/1e6:.1f} post_ms={g.dev_stats[7]/1e6:.1f} rechecks={g.dev_stats[1]} gen={tg:.1f}s", flush=True)
+              f"sum_nk2={float((g.sizes.astype(np.float64)**2).sum()):.3e} adj_ms={g.dev_stats[5]/1e6:.1f} pre_ms={g.dev_stats[6]/1e6:.1f} post_ms={g.dev_stats[7]/1e6:.1f} rechecks={g.dev_stats[1]} kept={1-g.dev_stats[2]/max(g.dev_stats[3],1):.3f} gen={tg:.1f}s", flush=True)

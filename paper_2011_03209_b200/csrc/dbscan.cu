@@ -27,12 +27,13 @@ namespace bm {
 bool tc_supported(int64_t d);
 struct TcPrep;
 int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
-               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out);
+               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
+               double* cen, double* rad);
 void tc_release(TcPrep* tp);
 int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
-              int64_t pairs, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
-              cudaStream_t stream);
+              int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
+              int64_t* stats, cudaStream_t stream);
 
 namespace {
 
@@ -74,10 +75,76 @@ struct GroupItem {
   int32_t k, e0, e1, pad;  // element, entries [e0, e1) (batch-relative)
 };
 
+// Seed order per grouped element: a greedy nearest-neighbour chain from
+// seed 0 over the seeds' first kGroupDims dims, so that consecutive groups
+// (and the tiles straddling their boundaries) are spatially close. One CTA
+// per element; rank[k * kGroupSeeds + s] = position of seed s in the chain.
+__global__ void __launch_bounds__(256)
+seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                  const int64_t* __restrict__ offs, const int32_t* __restrict__ elems,
+                  int32_t* __restrict__ rank) {
+  __shared__ float sd[kGroupSeeds][kGroupDims + 1];
+  __shared__ float dist[kGroupSeeds][kGroupSeeds + 1];
+  __shared__ int used[kGroupSeeds];
+  const int k = elems[blockIdx.x];
+  const int64_t ek = offs[k], nk = offs[k + 1] - ek;
+  const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
+  const int D = d < kGroupDims ? (int)d : kGroupDims;
+  for (int i = threadIdx.x; i < kGroupSeeds * kGroupDims; i += blockDim.x) {
+    const int j = i / kGroupDims, dim = i % kGroupDims;
+    sd[j][dim] = (j < S && dim < D) ? (float)X[rows[ek + (j * nk) / S] * d + dim] : 0.0f;
+  }
+  if (threadIdx.x < kGroupSeeds) used[threadIdx.x] = threadIdx.x >= S;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kGroupSeeds * kGroupSeeds; i += blockDim.x) {
+    const int a = i / kGroupSeeds, b = i % kGroupSeeds;
+    float acc = 0.0f;
+    for (int dim = 0; dim < D; ++dim) {
+      const float df = sd[a][dim] - sd[b][dim];
+      acc = fmaf(df, df, acc);
+    }
+    dist[a][b] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int cur = 0;
+    if (lane == 0) {
+      rank[(int64_t)k * kGroupSeeds] = 0;
+      used[0] = 1;
+    }
+    __syncwarp();
+    for (int step = 1; step < S; ++step) {
+      float best = 3.0e38f;
+      int bi = kGroupSeeds;
+      for (int c = lane; c < kGroupSeeds; c += 32)
+        if (!used[c] && (dist[cur][c] < best || (dist[cur][c] == best && c < bi))) {
+          best = dist[cur][c];
+          bi = c;
+        }
+      for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      cur = bi;
+      if (lane == 0) {
+        rank[(int64_t)k * kGroupSeeds + cur] = step;
+        used[cur] = 1;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128)
 group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                     const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
-                    uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+                    const int32_t* __restrict__ seed_rank, uint64_t* __restrict__ keys,
+                    int64_t* __restrict__ vals) {
   __shared__ float sd[kGroupDims][kGroupSeeds];  // seed coordinates, [dim][seed]
   const GroupItem it = items[blockIdx.x];
   const int64_t ek = offs[it.k], nk = offs[it.k + 1] - ek;
@@ -120,7 +187,7 @@ group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
       }
     }
     if (lane == 0) {
-      keys[e] = ((uint64_t)it.k << 7) | (uint64_t)bi;
+      keys[e] = ((uint64_t)it.k << 7) | (uint64_t)seed_rank[(int64_t)it.k * kGroupSeeds + bi];
       vals[e] = e;
     }
   }
@@ -215,7 +282,7 @@ tile_geom_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
       if (wmax[i] == wmax[i]) mm = fmax(mm, wmax[i]);
       else any_nan = true;
     }
-    rad[t] = any_nan ? __longlong_as_double(0x7ff8000000000000ll) : mm * (1.0 + 1e-12) + 1e-300;
+    rad[t] = any_nan ? __longlong_as_double(0x7ff8000000000000ll) : mm;
   }
 }
 
@@ -276,8 +343,9 @@ tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
       if (I >= T || J >= T || J < I) continue;
       int keep = 1;
       if (I != J) {
-        const double lb =
-            (sqrt(acc[a][b]) * (1.0 - 1e-12) - rad[tb + I] - rad[tb + J]) * (1.0 - gamma);
+        // radii: raw fp64 maxima of |x - c|, inflated far above their rounding error
+        const double rsum = (rad[tb + I] + rad[tb + J]) * (1.0 + 1e-12) + 1e-300;
+        const double lb = (sqrt(acc[a][b]) * (1.0 - 1e-12) - rsum) * (1.0 - gamma);
         keep = lb > eps ? 0 : 1;
       }
       flags[et.tp_off[k] + tri_index(I, J, T)] = keep;
@@ -464,7 +532,7 @@ template <int DEPTH>
 __global__ void __launch_bounds__(256, 1)
 adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, double eps,
                        const TileRef* __restrict__ tiles, uint32_t* __restrict__ adj,
-                       int64_t tile0) {
+                       int32_t* __restrict__ nonempty, int64_t tile0) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + kKC * kLd;
@@ -549,7 +617,13 @@ adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, 
   }
   __syncthreads();
   uint32_t* dst = adj + g * kTileWords;
-  for (int i = threadIdx.x; i < kTileWords; i += blockDim.x) dst[i] = bits[i];
+  int any = 0;
+  for (int i = threadIdx.x; i < kTileWords; i += blockDim.x) {
+    dst[i] = bits[i];
+    any |= bits[i] != 0u;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) nonempty[g] = any;
 }
 
 // ---------------------------------------------------------------------------
@@ -623,12 +697,14 @@ __global__ void __launch_bounds__(128)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
                   const TileUnit* __restrict__ units, const TileRef* __restrict__ tiles,
                   int64_t slot0, int64_t n_units, const uint8_t* __restrict__ core,
-                  int32_t* __restrict__ par, int32_t* __restrict__ bmin) {
+                  int32_t* __restrict__ par, int32_t* __restrict__ bmin,
+                  const int32_t* __restrict__ uni, const int32_t* __restrict__ nonempty) {
   __shared__ uint32_t bits[kTileWords];
   __shared__ int groot[2 * kTile];  // global root of each tile node (-1: not core)
   __shared__ int lp[2 * kTile];     // local union-find over tile nodes
   __shared__ uint32_t coreJ[4], coreI[4];
   __shared__ int any_merge;
+  __shared__ int rmm[4][4];  // per warp: min/max core root of rows, of columns
   const int t = threadIdx.x;
   for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     const TileUnit un = units[u];
@@ -644,10 +720,23 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
       const unsigned bi = __ballot_sync(0xffffffffu, ci);
       if ((t & 31) == 0) coreI[t >> 5] = bi;
     }
+    const int uI = DIAG ? -1 : uni[(pb >> 7) + I];
     for (int s = 0; s < un.cnt; ++s) {
       const int64_t g = un.off + s;
       const int J = tiles[g].J;
       const int pJ = (int)(pb + J * kTile);
+      if (!DIAG) {
+        if (!nonempty[g - slot0]) continue;  // no bit: nothing to join (block-uniform)
+        if (uI >= 0) {
+          // both tiles all-core with one root each: the tile's bits can only
+          // join the two roots (border rules need non-core rows: none here)
+          const int uJ = uni[(pb >> 7) + J];
+          if (uJ >= 0) {
+            if (t == 0 && uI != uJ) uf_union(par, uI, uJ);
+            continue;  // block-uniform
+          }
+        }
+      }
       __syncthreads();
       reinterpret_cast<uint4*>(bits)[t] =
           reinterpret_cast<const uint4*>(adj + (g - slot0) * kTileWords)[t];
@@ -657,14 +746,48 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         if ((t & 31) == 0) coreJ[t >> 5] = bj;
       }
       groot[t] = gr;
-      groot[kTile + t] = (!DIAG && cj) ? uf_find(par, pJ + t) : -1;
+      const int grj = (!DIAG && cj) ? uf_find(par, pJ + t) : -1;
+      groot[kTile + t] = grj;
       lp[t] = t;
       lp[kTile + t] = kTile + t;
       if (t == 0) any_merge = 0;
+      if (!DIAG) {  // per-warp min/max of the core roots of rows and columns
+        const int w = t >> 5;
+        const unsigned mnI = __reduce_min_sync(0xffffffffu, ci ? (unsigned)gr : 0x7fffffffu);
+        const int mxI = __reduce_max_sync(0xffffffffu, ci ? gr : -1);
+        const unsigned mnJ = __reduce_min_sync(0xffffffffu, cj ? (unsigned)grj : 0x7fffffffu);
+        const int mxJ = __reduce_max_sync(0xffffffffu, cj ? grj : -1);
+        if ((t & 31) == 0) {
+          rmm[0][w] = (int)mnI;
+          rmm[1][w] = mxI;
+          rmm[2][w] = (int)mnJ;
+          rmm[3][w] = mxJ;
+        }
+      }
       __syncthreads();
-      // --- core-core edges between nodes with different global roots
       const int r = t;
-      if (ci) {
+      bool uniform = false;
+      if (!DIAG) {
+        // every core row in one (possibly stale) root RI and every core column
+        // in one root RJ: one union(RI, RJ) covers all core-core bits
+        const int mnI = min(min(rmm[0][0], rmm[0][1]), min(rmm[0][2], rmm[0][3]));
+        const int mxI = max(max(rmm[1][0], rmm[1][1]), max(rmm[1][2], rmm[1][3]));
+        const int mnJ = min(min(rmm[2][0], rmm[2][1]), min(rmm[2][2], rmm[2][3]));
+        const int mxJ = max(max(rmm[3][0], rmm[3][1]), max(rmm[3][2], rmm[3][3]));
+        uniform = (mxI < 0 || mnI == mxI) && (mxJ < 0 || mnJ == mxJ);
+        if (uniform) {
+          const bool hit = ci && (((bits[r * 4] & coreJ[0]) | (bits[r * 4 + 1] & coreJ[1]) |
+                                   (bits[r * 4 + 2] & coreJ[2]) | (bits[r * 4 + 3] & coreJ[3])) != 0u);
+          const int any = __syncthreads_or(hit && mnI != mnJ);
+          if (any) {
+            if (t == 0) uf_union(par, mnI, mnJ);
+            __syncthreads();
+            if (ci) gr = uf_find(par, gr);
+          }
+        }
+      }
+      // --- core-core edges between nodes with different global roots
+      if (ci && !uniform) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
@@ -713,6 +836,34 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         if (ci) gr = uf_find(par, gr);  // refresh the row roots after merges
       }
     }
+  }
+}
+
+// per 128-row tile: the common root of its rows if every valid row is core
+// and all share one root (stale roots are fine: still in the component), else -1
+__global__ void tile_uniform_kernel(ElemTables et, int64_t n_rt, const uint8_t* __restrict__ core,
+                                    int32_t* __restrict__ par, int32_t* __restrict__ uni) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t rt = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); rt < n_rt;
+       rt += (int64_t)gridDim.x * wpb) {
+    bool ok = true;
+    int mn = 0x7fffffff, mx = -1;
+    for (int i = lane; i < kTile; i += 32) {
+      const int64_t p = rt * kTile + i;
+      if (et.ent[p] < 0) continue;
+      if (!core[p]) {
+        ok = false;
+        continue;
+      }
+      const int r = uf_find(par, (int)p);
+      mn = min(mn, r);
+      mx = max(mx, r);
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) uni[rt] = (ok && mx >= 0 && mn == mx) ? mn : -1;
   }
 }
 
@@ -787,7 +938,8 @@ inline unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
 
 template <int DEPTH>
 int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
-                       int64_t n_tiles, double eps, uint32_t* adj, cudaStream_t stream) {
+                       int64_t n_tiles, double eps, uint32_t* adj, int32_t* nonempty,
+                       cudaStream_t stream) {
   static bool attr_done = false;  // per process; attribute is per function
   if (!attr_done) {
     BM_CHECK_CUDA(cudaFuncSetAttribute(adjacency_exact_kernel<DEPTH>,
@@ -798,26 +950,27 @@ int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const 
   const int64_t kMaxGrid = 1ll << 30;
   for (int64_t t0 = 0; t0 < n_tiles; t0 += kMaxGrid) {
     int64_t nb = std::min<int64_t>(kMaxGrid, n_tiles - t0);
-    adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(Xg, d, et, eps,
-                                                                            tiles, adj, t0);
+    adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(
+        Xg, d, et, eps, tiles, adj, nonempty, t0);
     BM_CHECK_LAUNCH();
   }
   return BM_OK;
 }
 
 int exact_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
-                          int64_t n_tiles, double eps, uint32_t* adj, cudaStream_t stream) {
+                          int64_t n_tiles, double eps, uint32_t* adj, int32_t* nonempty,
+                          cudaStream_t stream) {
   if (n_tiles == 0) return BM_OK;
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
   BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
                                         stream));
   switch (prog.depth) {
-    case 1: return launch_exact_depth<1>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
-    case 2: return launch_exact_depth<2>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
-    case 3: return launch_exact_depth<3>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
-    case 4: return launch_exact_depth<4>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
-    default: return launch_exact_depth<kMaxStack>(Xg, d, et, tiles, n_tiles, eps, adj, stream);
+    case 1: return launch_exact_depth<1>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
+    case 2: return launch_exact_depth<2>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
+    case 3: return launch_exact_depth<3>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
+    case 4: return launch_exact_depth<4>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
+    default: return launch_exact_depth<kMaxStack>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
   }
 }
 
@@ -872,7 +1025,7 @@ struct BatchCtx {
   // n_kept), first off-diagonal / tensor-core unit (n_rt+1), row pairs
   int64_t n_kept = 0;
   std::vector<int64_t> row_first, off_pos, tc_pos, row_pairs;
-  Scratch tabs, xg, work, perm, s_tiles, s_units;
+  Scratch tabs, xg, work, perm, s_tiles, s_units, s_geo;
   TileRef* d_tiles = nullptr;
   TileUnit *d_diag = nullptr, *d_off = nullptr, *d_tcu = nullptr;
   ElemTables et{};
@@ -961,11 +1114,23 @@ struct BatchCtx {
         BM_CHECK_LAUNCH();
       }
       if (!items.empty()) {
+        std::vector<int32_t> gel;
+        for (int64_t i = 0; i < nb_el; ++i)
+          if (nrows[i] >= min_rows) gel.push_back((int32_t)i);
+        Scratch s_rank, s_gel;
+        BM_TRY(scratch_alloc(s_rank, (size_t)nb_el * kGroupSeeds * 4, stream));
+        BM_TRY(scratch_alloc(s_gel, gel.size() * 4, stream));
+        BM_CHECK_CUDA(cudaMemcpyAsync(s_gel.ptr, gel.data(), gel.size() * 4,
+                                      cudaMemcpyHostToDevice, stream));
+        seed_order_kernel<<<(unsigned)gel.size(), 256, 0, stream>>>(
+            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>());
+        BM_CHECK_LAUNCH();
         BM_TRY(scratch_alloc(s_it, items.size() * sizeof(GroupItem), stream));
         BM_CHECK_CUDA(cudaMemcpyAsync(s_it.ptr, items.data(), items.size() * sizeof(GroupItem),
                                       cudaMemcpyHostToDevice, stream));
         group_assign_kernel<<<(unsigned)items.size(), 128, 0, stream>>>(
-            d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_k.as<uint64_t>(), s_v.as<int64_t>());
+            d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_rank.as<int32_t>(),
+            s_k.as<uint64_t>(), s_v.as<int64_t>());
         BM_CHECK_LAUNCH();
         int bits = 7;
         while (bits < 64 && ((uint64_t)nb_el << 7) >> bits) ++bits;
@@ -995,10 +1160,16 @@ struct BatchCtx {
     core = (uint8_t*)(hscan + P + 1);
     BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
-    if (use_tc) BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc));
+    // tile centres / radii for the pruning bound: fused into the tensor-core
+    // engine's quantisation pass, else a separate pass (build_tiles)
+    if (prune) BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
+    double* cen = prune ? s_geo.as<double>() : nullptr;
+    double* rad = prune ? cen + n_rt * d : nullptr;
+    if (use_tc) BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad));
 
     // ---- kept tile pairs and work units (device-built)
     BM_TRY(build_tiles(d_tbase, prune));
+    s_geo.release();
     stats[3] += n_tp;
     stats[2] += n_tp - n_kept;
     return BM_OK;
@@ -1019,13 +1190,14 @@ struct BatchCtx {
     BM_TRY(scratch_alloc(s_fl, (size_t)n_tp * 4, stream));
     int32_t* flags = s_fl.as<int32_t>();
     if (prune) {
-      Scratch s_geo, s_blk;
-      BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
+      Scratch s_blk;
       double* cen = s_geo.as<double>();
       double* rad = cen + n_rt * d;
-      tile_geom_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(xg.as<double>(), d, et,
-                                                           s_re.as<int32_t>(), cen, rad);
-      BM_CHECK_LAUNCH();
+      if (!use_tc) {
+        tile_geom_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(xg.as<double>(), d, et,
+                                                             s_re.as<int32_t>(), cen, rad);
+        BM_CHECK_LAUNCH();
+      }
       const int64_t nblk = (int64_t)blocks.size();
       BM_TRY(scratch_alloc(s_blk, (size_t)nblk * sizeof(PruneBlock), stream));
       BM_CHECK_CUDA(cudaMemcpyAsync(s_blk.ptr, blocks.data(), nblk * sizeof(PruneBlock),
@@ -1128,12 +1300,13 @@ struct BatchCtx {
   int adjacency(int32_t I0, int32_t I1, uint32_t* adj, int32_t* cnt_acc, int64_t* stats) {
     WindowBufs w;
     BM_TRY(window(I0, I1, w));
+    int32_t* nonempty = reinterpret_cast<int32_t*>(adj + w.n_tiles * kTileWords);
     if (use_tc) {
       BM_TRY(tc_window(tc, xg.as<double>(), et, w.tiles, w.slot0, w.n_tiles, w.tcu, w.n_tc,
-                       w.pairs, adj, cnt_acc, I0 >= 0, stats, stream));
+                       w.pairs, adj, nonempty, cnt_acc, I0 >= 0, stats, stream));
     } else {
       BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, w.tiles + w.slot0, w.n_tiles, eps,
-                                   adj, stream));
+                                   adj, nonempty, stream));
       if (cnt_acc) {
         if (w.n_diag > 0) {
           count_kernel<<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
@@ -1160,19 +1333,27 @@ struct BatchCtx {
   }
 
   // union-find over the core-core bits and border minima of the window
-  int components(int32_t I0, int32_t I1, const uint32_t* adj, int32_t* par_w, int32_t* bmin_w) {
+  // (adj: the window's bitmap followed by its per-slot nonempty flags)
+  int components(int32_t I0, int32_t I1, uint32_t* adj, int32_t* par_w, int32_t* bmin_w) {
     WindowBufs w;
     BM_TRY(window(I0, I1, w));
+    int32_t* nonempty = reinterpret_cast<int32_t*>(adj + w.n_tiles * kTileWords);
     if (w.n_diag > 0) {
       components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
-          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w);
+          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty);
       BM_CHECK_LAUNCH();
     }
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
     BM_CHECK_LAUNCH();
     if (w.n_off > 0) {
+      Scratch s_uni;
+      BM_TRY(scratch_alloc(s_uni, (size_t)n_rt * 4, stream));
+      tile_uniform_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(et, n_rt, core, par_w,
+                                                                     s_uni.as<int32_t>());
+      BM_CHECK_LAUNCH();
       components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
-          adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w);
+          adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w, s_uni.as<int32_t>(),
+          nonempty);
       BM_CHECK_LAUNCH();
     }
     return BM_OK;
@@ -1182,7 +1363,7 @@ struct BatchCtx {
   size_t window_bytes(int32_t I0, int32_t I1) const {
     int64_t r0 = 0, r1 = 0;
     rows_of(I0, I1, r0, r1);
-    return (size_t)std::max<int64_t>(row_first[r1] - row_first[r0], 1) * kTileWords * 4;
+    return (size_t)std::max<int64_t>(row_first[r1] - row_first[r0], 1) * (kTileWords * 4 + 4);
   }
 
   // canonical labels of every entry (element-relative cluster ids, -1 noise)

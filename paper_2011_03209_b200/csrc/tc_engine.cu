@@ -197,6 +197,7 @@ struct TcParams {
   double a3max;           // 2^9 * 2 * 255^2 * Kpad (bound of the A3 term in D2)
   int nkc;                // Kpad / 128
   uint32_t* adj;
+  int32_t* nonempty;      // per window slot: 1 if the tile holds any bit (zeroed by the host)
   int32_t* cnt;           // eps-neighbour counts per padded row (self included)
   int4* queue;            // undecided pairs: (p_i, p_j, slot, element)
   const uint8_t* planes;  // limb planes [3][P][kpad]
@@ -629,6 +630,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         // bitmap words (row, 2 x 32 columns) of tile (I, J)
         *reinterpret_cast<uint2*>(P.adj + tile * kTileWords + row * 4 + ch * 2) =
             make_uint2(in_w[0], in_w[1]);
+        if (__any_sync(0xffffffffu, (in_w[0] | in_w[1]) != 0u) && lane == 0)
+          P.nonempty[tile] = 1;
         row_count += __popc(in_w[0]) + __popc(in_w[1]);
         // column counts (off-diagonal tiles only): 32x32 bit transposes across
         // the warp (lane j then holds column j), popc, reduce the 4 row
@@ -711,24 +714,28 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
 // ---------------------------------------------------------------------------
 // preparation: per-element centre / scale, quantisation, per-tile error max
 // ---------------------------------------------------------------------------
-// per 128-row tile (global tile index t): column min/max over valid rows
+// per 128-row tile (global tile index t): column min/max over valid rows, and
+// (when cen != null) the tile centre = column means, for the pruning bound
 __global__ void tile_minmax_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
                                    const int32_t* __restrict__ tile_elem, int64_t n_tiles,
-                                   double* __restrict__ tmin, double* __restrict__ tmax) {
+                                   double* __restrict__ tmin, double* __restrict__ tmax,
+                                   double* __restrict__ cen) {
   const int64_t t = blockIdx.x;
   if (t >= n_tiles) return;
   const int k = tile_elem[t];
   const int64_t p0 = t * kTile;  // padded base of this tile
   const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn, sm = 0.0;
     for (int r = 0; r < valid; ++r) {
       const double v = Xg[(p0 + r) * d + c];
       mn = fmin(mn, v);
       mx = fmax(mx, v);
+      sm += v;
     }
     tmin[t * d + c] = mn;
     tmax[t * d + c] = mx;
+    if (cen) cen[t * d + c] = sm / (double)valid;
   }
 }
 
@@ -764,13 +771,17 @@ __global__ void elem_scale_kernel(int64_t d, ElemTables et, const int32_t* __res
   }
 }
 
-// one warp per padded row: limbs into the three planes, N = sum q^2 (exact),
-// e = |x - c - s q| (fp64) -> tile max via atomicMax on the bit pattern
+// one warp per padded row: limbs into the three planes (4 columns per lane,
+// packed 32-bit stores), N = sum q^2 (exact), e = |x - c - s q| (fp64) -> tile
+// max via atomicMax on the bit pattern; with cen != null also the row's
+// distance to its tile centre -> tile radius (raw max, NaN-propagating)
 __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad,
                                 ElemTables et, int64_t P, const double* __restrict__ center,
                                 const double* __restrict__ scale, int8_t* __restrict__ planes,
                                 int64_t* __restrict__ nq, int32_t* __restrict__ cq,
-                                unsigned long long* __restrict__ tile_e) {
+                                unsigned long long* __restrict__ tile_e,
+                                const double* __restrict__ cen,
+                                unsigned long long* __restrict__ rad_bits) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
@@ -784,31 +795,45 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
     const bool valid = (p - et.pbase[k]) < et.nrows[k];
     const double s = scale[k];
     const double inv = 1.0 / s;
+    const double* xr = Xg + p * d;
+    const double* ck = center + (int64_t)k * d;
+    const double* ct = cen ? cen + (p / kTile) * d : nullptr;
     long long nsum = 0;
-    double esum = 0.0, ysum = 0.0;
-    int8_t* hp = planes + p * kpad;
-    uint8_t* mp = (uint8_t*)planes + P * kpad + p * kpad;
-    uint8_t* lp = (uint8_t*)planes + 2 * P * kpad + p * kpad;
-    for (int64_t c = lane; c < kpad; c += 32) {
-      int q = 0;
-      if (valid && c < d) {
-        const double y = Xg[p * d + c] - center[(int64_t)k * d + c];
-        double qd = rint(y * inv);
-        qd = fmin(fmax(qd, -(double)((1 << kQBits) - 1)), (double)((1 << kQBits) - 1));
-        q = (int)qd;
-        const double e = y - qd * s;
-        esum += e * e;
-        ysum += y * y;
+    double esum = 0.0, ysum = 0.0, rsum = 0.0;
+    for (int64_t c4 = 4 * lane; c4 < kpad; c4 += 128) {
+      uint32_t hw = 0, mw = 0, lw = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = c4 + j;
+        int q = 0;
+        if (valid && c < d) {
+          const double x = xr[c];
+          const double y = x - ck[c];
+          double qd = rint(y * inv);
+          qd = fmin(fmax(qd, -(double)((1 << kQBits) - 1)), (double)((1 << kQBits) - 1));
+          q = (int)qd;
+          const double e = y - qd * s;
+          esum += e * e;
+          ysum += y * y;
+          if (ct) {
+            const double dr = x - ct[c];
+            rsum += dr * dr;
+          }
+        }
+        nsum += (long long)q * q;
+        hw |= (uint32_t)(uint8_t)(int8_t)(q >> (2 * kLimb)) << (8 * j);
+        mw |= (uint32_t)((q >> kLimb) & ((1 << kLimb) - 1)) << (8 * j);
+        lw |= (uint32_t)(q & ((1 << kLimb) - 1)) << (8 * j);
       }
-      nsum += (long long)q * q;
-      hp[c] = (int8_t)(q >> (2 * kLimb));
-      mp[c] = (uint8_t)((q >> kLimb) & ((1 << kLimb) - 1));
-      lp[c] = (uint8_t)(q & ((1 << kLimb) - 1));
+      *reinterpret_cast<uint32_t*>(planes + p * kpad + c4) = hw;
+      *reinterpret_cast<uint32_t*>(planes + P * kpad + p * kpad + c4) = mw;
+      *reinterpret_cast<uint32_t*>(planes + 2 * P * kpad + p * kpad + c4) = lw;
     }
     for (int o = 16; o; o >>= 1) {
       nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       esum += __shfl_xor_sync(0xffffffffu, esum, o);
       ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
+      rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
     }
     if (lane == 0) {
       nq[p] = nsum;
@@ -818,6 +843,11 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
         // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
         const double e = sqrt(esum) * (1.0 + 1e-12) + 1e-15 * sqrt(ysum) + 1e-300;
         atomicMax(tile_e + p / kTile, (unsigned long long)__double_as_longlong(e));
+        if (rad_bits) {
+          const double rr = sqrt(rsum);  // NaN (positive) sorts above every finite value
+          atomicMax(rad_bits + p / kTile,
+                    (unsigned long long)__double_as_longlong(rr == rr ? rr : __longlong_as_double(0x7ff8000000000000ll)));
+        }
       }
     }
   }
@@ -844,13 +874,15 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
 }
 
 __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
-                                           uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
+                                           uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
+                                           int32_t* __restrict__ cnt,
                                            unsigned long long* __restrict__ n_inside) {
   const int k = pr.w;
   const int li = pr.x - et.pbase[k], lj = pr.y - et.pbase[k];
   const int I = li / kTile, J = lj / kTile, r = li % kTile, c = lj % kTile;
   const int64_t tile = pr.z;
   atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
+  nonempty[tile] = 1;
   atomicAdd(cnt + pr.x, 1);
   if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
   atomicAdd(n_inside, 1ull);
@@ -867,10 +899,12 @@ __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
 // statically; the leaf walk is uniform across lanes.
 constexpr int kRcWarps = 4;
 
-__global__ void __launch_bounds__(kRcWarps * 32)
+template <int DEPTH>
+__global__ void __launch_bounds__(kRcWarps * 32, 6)
     recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
                    const int4* __restrict__ queue, int64_t nq, double eps,
-                   uint32_t* __restrict__ adj, int32_t* __restrict__ cnt,
+                   uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
+                   int32_t* __restrict__ cnt,
                    unsigned long long* __restrict__ n_inside) {
   __shared__ double sq_all[kRcWarps][32][33];
   const int lane = threadIdx.x & 31;
@@ -885,24 +919,31 @@ __global__ void __launch_bounds__(kRcWarps * 32)
     const int np = (nq - base) < 32 ? (int)(nq - base) : 32;
     double s_seq = 0.0, res = 0.0;
     double r[8];
-    PwStack st;
+    double st[DEPTH];  // pairwise partial sums (register stack, static indexing)
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = 0.0;
 #pragma unroll
-    for (int j = 0; j < kMaxStack; ++j) st.s[j] = 0.0;
+    for (int j = 0; j < DEPTH; ++j) st[j] = 0.0;
     int li = 0;
     for (int64_t c0 = 0; c0 < d; c0 += 32) {
       const bool cv = c0 + lane < d;
-#pragma unroll 4
-      for (int p = 0; p < np; ++p) {
-        const int64_t ra = __shfl_sync(0xffffffffu, pr.x, p);
-        const int64_t rb = __shfl_sync(0xffffffffu, pr.y, p);
-        double v = 0.0;
-        if (cv) {
-          const double df = __dsub_rn(Xg[ra * d + c0 + lane], Xg[rb * d + c0 + lane]);
-          v = __dmul_rn(df, df);
+      // 8 pairs per step: all 16 row loads issued before any is consumed
+      for (int p0 = 0; p0 < np; p0 += 8) {
+        double va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int p = p0 + u;
+          const int64_t ra = __shfl_sync(0xffffffffu, pr.x, p & 31);
+          const int64_t rb = __shfl_sync(0xffffffffu, pr.y, p & 31);
+          const bool ok = cv && p < np;
+          va[u] = ok ? __ldg(Xg + ra * d + c0 + lane) : 0.0;
+          vb[u] = ok ? __ldg(Xg + rb * d + c0 + lane) : 0.0;
         }
-        S[p][lane] = v;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double df = __dsub_rn(va[u], vb[u]);
+          S[(p0 + u) & 31][lane] = __dmul_rn(df, df);
+        }
       }
       __syncwarp();
 #pragma unroll
@@ -942,16 +983,22 @@ __global__ void __launch_bounds__(kRcWarps * 32)
           finish = true;
         }
         if (finish) {
-          st.push(res);
-          for (int q = 0; q < L.pops; ++q) st.reduce();
+#pragma unroll
+          for (int j = DEPTH - 1; j > 0; --j) st[j] = st[j - 1];
+          st[0] = res;
+          for (int q = 0; q < L.pops; ++q) {
+            st[0] = __dadd_rn(st[1 < DEPTH ? 1 : 0], st[0]);
+#pragma unroll
+            for (int j = 1; j < DEPTH - 1; ++j) st[j] = st[j + 1];
+          }
           ++li;
         }
       }
       __syncwarp();
     }
     if (have) {
-      const double s2 = et.order[k] == BM_ORDER_SEQUENTIAL ? s_seq : __dadd_rn(0.0, st.s[0]);
-      if (__dsqrt_rn(s2) <= eps) set_inside(et, pr, adj, cnt, n_inside);
+      const double s2 = et.order[k] == BM_ORDER_SEQUENTIAL ? s_seq : __dadd_rn(0.0, st[0]);
+      if (__dsqrt_rn(s2) <= eps) set_inside(et, pr, adj, nonempty, cnt, n_inside);
     }
   }
 }
@@ -1006,7 +1053,7 @@ bool tc_supported(int64_t d) { return d >= 32 && d <= 256; }
 // tile rows, twice: counts, then components).
 struct TcPrep {
   int64_t d = 0, P = 0, n_el = 0, n_tiles = 0, kpad = 0;
-  int nkc = 0;
+  int nkc = 0, depth = 1;  // depth: pairwise-sum stack depth of d (PwProgram)
   double eps = 0.0;
   std::vector<int32_t> nrows;
   Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw;
@@ -1019,7 +1066,8 @@ struct TcPrep {
 };
 
 int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
-               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out) {
+               const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
+               double* cen, double* rad) {
   *out = nullptr;
   const int64_t kpad = ceil_div(d, kKC) * kKC;
   const int nkc = (int)(kpad / kKC);
@@ -1039,6 +1087,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   tp->n_el = n_el;
   tp->kpad = kpad;
   tp->nkc = nkc;
+  tp->depth = prog.depth;
   tp->eps = eps;
   tp->nrows = h_nrows;
   const int64_t n_tiles = P / kTile;
@@ -1068,14 +1117,16 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_te.ptr, 0, n_tiles * 8, stream));
 
   tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, tp->d_tile_elem, n_tiles,
-                                                            tmin, tmax);
+                                                            tmin, tmax, cen);
   BM_CHECK_LAUNCH();
   elem_scale_kernel<<<(unsigned)n_el, 256, 0, stream>>>(d, et, tp->d_tbase, tmin, tmax, center,
                                                         scale);
   BM_CHECK_LAUNCH();
+  if (rad) BM_CHECK_CUDA(cudaMemsetAsync(rad, 0, n_tiles * 8, stream));
   quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
       Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
-      reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>());
+      reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
+      cen, reinterpret_cast<unsigned long long*>(rad));
   BM_CHECK_LAUNCH();
   BM_TRY(make_qmap(&tp->qmap, tp->s_pl.ptr, P, kpad));
 
@@ -1112,8 +1163,8 @@ __global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __re
 // pairs = distinct row pairs inside the window's tiles (stats and queue size).
 int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
-              int64_t pairs, uint32_t* adj, int32_t* cnt, bool accumulate, int64_t* stats,
-              cudaStream_t stream) {
+              int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
+              int64_t* stats, cudaStream_t stream) {
   const int64_t P = tp->P, d = tp->d;
   const int nkc = tp->nkc;
   if (n_units == 0) return BM_OK;
@@ -1144,6 +1195,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     BM_TRY(scratch_alloc(s_q, qcap * sizeof(int4), stream));
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(nonempty, 0, (size_t)n_tiles * 4, stream));
     TcParams prm{};
     prm.et = et;
     prm.units = units;
@@ -1161,6 +1213,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     prm.a3max = (double)(2 << kLimb) * 2.0 * lmax * lmax * (double)tp->kpad;  // 2^(b+1) A3
     prm.nkc = nkc;
     prm.adj = adj;
+    prm.nonempty = nonempty;
     prm.cnt = cnt_run;
     prm.queue = s_q.as<int4>();
     prm.planes = tp->s_pl.as<uint8_t>();
@@ -1216,8 +1269,22 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   }
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
-    recheck_kernel<<<grid_cap(nrec, kRcWarps * 32, 8), kRcWarps * 32, 0, stream>>>(
-        Xg, d, et, s_q.as<int4>(), nrec, tp->eps, adj, cnt_run, d_cnt + 1);
+    const unsigned rg = grid_cap(nrec, kRcWarps * 32, 6);
+    const int4* q = s_q.as<int4>();
+    switch (tp->depth) {
+      case 1:
+        recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
+                                                            nonempty, cnt_run, d_cnt + 1);
+        break;
+      case 2:
+        recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
+                                                            nonempty, cnt_run, d_cnt + 1);
+        break;
+      default:
+        recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
+                                                            nonempty, cnt_run, d_cnt + 1);
+        break;
+    }
     BM_CHECK_LAUNCH();
   }
   if (accumulate && cnt) {

@@ -51,8 +51,9 @@ constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
 constexpr int kStages = 2;      // B ring depth (full-K B tiles)
 constexpr int kUnitB = 32;      // B (= bitmap) tiles per work unit
 constexpr int kInfo = 3;        // per-tile info ring depth (smem)
-constexpr int kEpiWarps = 8;    // epilogue warps 4..11
-constexpr int kLoadWarps = 4;   // A-loader warps 12..15
+constexpr int kEpiWarps = 16;   // epilogue warps 4..19 (4 per TMEM lane quarter)
+constexpr int kEpiCols = kBN / (kEpiWarps / 4);  // columns per epilogue warp (32)
+constexpr int kLoadWarps = 4;   // A-loader warps 20..23
 constexpr int kThreads = 128 + 32 * (kEpiWarps + kLoadWarps);
 constexpr int kLimb = 7;        // bits of the M and L limbs
 constexpr int kQBits = 2 * kLimb + 7;   // |q| <= 2^21 - 1: H = q >> 14 is a signed byte
@@ -314,15 +315,15 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
   uint64_t* acc_full = b_empty + kStages;     // [2]: (A0, A1), A2
   uint64_t* acc_empty = acc_full + 2;         // [2]
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
-  int32_t* colcnt = (int32_t*)(tmem_slot + 4);            // [2][kBN]
   // per-tile info ring, filled ahead by the producer: floor(N_j/U) of the
   // tile's 128 columns (bulk TMA) + the tile's integer threshold offsets
   struct TileInfo {
     int32_t cq[kBN];
     int2 th;
-    int2 pad;
+    int32_t J;  // column tile
+    int32_t pad;
   };
-  TileInfo* info = (TileInfo*)(((uintptr_t)(colcnt + 2 * kBN) + 15) & ~(uintptr_t)15);
+  TileInfo* info = (TileInfo*)(((uintptr_t)(tmem_slot + 4) + 15) & ~(uintptr_t)15);
   uint64_t* info_full = (uint64_t*)(info + kInfo);        // [kInfo]
   uint64_t* info_empty = info_full + kInfo;               // [kInfo]
 
@@ -345,7 +346,6 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < 2 * kBN; i += blockDim.x) colcnt[i] = 0;
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tmem_slot)));
@@ -380,6 +380,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
           mbar_wait(info_empty + islot, ph_info[islot] ^ 1);
           ph_info[islot] ^= 1;
           info[islot].th = *reinterpret_cast<const int2*>(P.thr + (un.off + t - P.slot0));
+          info[islot].J = b;
           mbar_expect_tx(info_full + islot, kBN * 4);
           bulk_load(info[islot].cq, P.cq + pb + b * kBN, kBN * 4, info_full + islot);
           islot = (islot + 1) % kInfo;
@@ -518,31 +519,41 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    // warp (q, ch): TMEM lane quarter q (rows 32q..32q+31), column half ch (64 columns)
+    // warp (q, ch): TMEM lane quarter q (rows 32q..32q+31), column quarter ch
+    // (kEpiCols = 32 columns). Row counts here; column counts of the
+    // off-diagonal tiles by colcount_kernel from the stored bits.
     const int ew = warp - 4;
     const int q = warp & 3;            // tcgen05.ld lane window = warp % 4
     const int ch = ew >> 2;
     const int row = q * 32 + lane;
     uint32_t ph_acc[2] = {0, 0};
-    uint32_t cbank = 0;                // colcnt double buffer
     uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
 #ifdef BM_TC_PROFILE
     long long ep[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long ep_t0 = clock64();
 #endif
+    // the next unit's descriptor and row data are fetched one unit ahead
+    // (dependent global loads off the per-tile critical path)
+    TileUnit un_nx = blockIdx.x < P.n_units ? P.units[blockIdx.x] : TileUnit{0, 0, 0, 0};
+    int pb_nx = P.et.pbase[un_nx.k], nk_nx = P.et.nrows[un_nx.k];
+    int32_t cq_nx = (int32_t)(P.nq[pb_nx + un_nx.I * kBM + row] >> kYShift);
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
-      const TileUnit un = P.units[u];
+      const TileUnit un = un_nx;
       const int k = un.k;
-      const int pb = P.et.pbase[k];
-      const int n_k = P.et.nrows[k];
+      const int pb = pb_nx;
+      const int n_k = nk_nx;
       const int gi = un.I * kBM + row;                // local row index
       const bool row_ok = gi < n_k;
-      const int niU = (int)(P.nq[pb + gi] >> kYShift);
+      const int niU = cq_nx;
+      if (u + gridDim.x < P.n_units) {
+        un_nx = P.units[u + gridDim.x];
+        pb_nx = P.et.pbase[un_nx.k];
+        nk_nx = P.et.nrows[un_nx.k];
+        cq_nx = (int32_t)(P.nq[pb_nx + un_nx.I * kBM + row] >> kYShift);
+      }
       int row_count = 0;
       for (int t = 0; t < un.cnt; ++t) {
-        const int J = P.tiles[un.off + t].J;
         const int64_t tile = un.off + t - P.slot0;    // window slot of the kept tile
-        const int col0 = J * kBN + ch * 64;           // first local column of this warp
         // Integer decision. With y = 2^7 a0 + a1 + (a2 >> 7) - floor(N_j/U):
         //   y >= r_in  => D2c <= t_in (certainly inside; a3, L.L >= 0)
         //   y <= r_out => D2c >  t_out (certainly outside; a3, L.L bounded)
@@ -553,8 +564,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         mbar_wait(info_full + islot, ph_info[islot]);
         ph_info[islot] ^= 1;
         const int2 th = info[islot].th;
-        const int cown0 = info[islot].cq[ch * 64 + lane];
-        const int cown1 = info[islot].cq[ch * 64 + 32 + lane];
+        const int J = info[islot].J;
+        const int col0 = J * kBN + ch * kEpiCols;     // first local column of this warp
+        const int cown = info[islot].cq[ch * kEpiCols + lane];
         __syncwarp();
         if (lane == 0) mbar_arrive(info_empty + islot);
         islot = (islot + 1) % kInfo;
@@ -562,16 +574,15 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         // keeps every decision and rules out int32 overflow below
         const int rin1 = th.x == kNever ? kYMax + 2 : max(-kYMax - 2, min(kYMax + 2, niU + th.x - 1));
         const int ro1 = th.y == kNever ? -kYMax - 2 : max(-kYMax - 2, min(kYMax + 2, niU + th.y + 1));
-        const uint32_t colmask0 = __ballot_sync(0xffffffffu, col0 + lane < n_k);
-        const uint32_t colmask1 = __ballot_sync(0xffffffffu, col0 + 32 + lane < n_k);
-        const uint32_t tq = tacc0 + ((uint32_t)(q * 32) << 16) + ch * 64;
-        // --- phase 1: t1 = 256 a0 + a1 (exact int32), then release A0/A1
+        const uint32_t colmask = __ballot_sync(0xffffffffu, col0 + lane < n_k);
+        const uint32_t tq = tacc0 + ((uint32_t)(q * 32) << 16) + ch * kEpiCols;
+        // --- phase 1: t1 = 2^7 a0 + a1 (exact int32), then release A0/A1
         mbar_wait(acc_full + 0, ph_acc[0]);
         EP_MARK(0);
         tc_fence_after();
-        int32_t t1[64];
+        int32_t t1[kEpiCols];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < kEpiCols / 16; ++h) {
           int32_t x0[16], x1[16];
           tmem_ld16(tq + 0 * kBN + h * 16, x0);
           tmem_ld16(tq + 1 * kBN + h * 16, x1);
@@ -582,14 +593,14 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + 0);
-        // --- phase 2: fold A2 into t1 (u = t1 + (a2 >> 8)), release A2 at once,
+        // --- phase 2: fold A2 into t1 (t1 + (a2 >> 7)), release A2 at once,
         //     then decide from registers while the next tile's MMAs run
         EP_MARK(2);
         mbar_wait(acc_full + 1, ph_acc[1]);
         EP_MARK(1);
         tc_fence_after();
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < kEpiCols / 16; ++h) {
           int32_t a2[16];
           tmem_ld16(tq + 2 * kBN + h * 16, a2);
           tmem_ld_wait();
@@ -599,72 +610,37 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + 1);
+        ph_acc[0] ^= 1;
+        ph_acc[1] ^= 1;
 
         // Decision per pair from two sign bits (no predicates, no selects):
         //   (r_in - 1) - y < 0  <=> certainly inside
         //   y - (r_out + 1) < 0 <=> certainly outside
-        // each funnel-shifted into a row word (columns 31..0 -> bits 31..0);
+        // each funnel-shifted into the row word (columns 31..0 -> bits 31..0);
         // neither => undecided -> exact recheck queue.
-        uint32_t in_w[2], amb_w[2];
         EP_MARK(3);
+        uint32_t wi_hi = 0, wi_lo = 0, wo_hi = 0, wo_lo = 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int cown = h ? cown1 : cown0;
-          uint32_t wi_hi = 0, wi_lo = 0, wo_hi = 0, wo_lo = 0;
-#pragma unroll
-          for (int jj = 15; jj >= 0; --jj) {
-            const int y_hi = t1[h * 32 + 16 + jj] - __shfl_sync(0xffffffffu, cown, 16 + jj);
-            const int y_lo = t1[h * 32 + jj] - __shfl_sync(0xffffffffu, cown, jj);
-            wi_hi = __funnelshift_l((uint32_t)(rin1 - y_hi), wi_hi, 1);
-            wi_lo = __funnelshift_l((uint32_t)(rin1 - y_lo), wi_lo, 1);
-            wo_hi = __funnelshift_l((uint32_t)(y_hi - ro1), wo_hi, 1);
-            wo_lo = __funnelshift_l((uint32_t)(y_lo - ro1), wo_lo, 1);
-          }
-          const uint32_t valid = row_ok ? (h ? colmask1 : colmask0) : 0u;
-          const uint32_t iw = (wi_hi << 16) | wi_lo, ow = (wo_hi << 16) | wo_lo;
-          in_w[h] = iw & valid;
-          amb_w[h] = valid & ~iw & ~ow;
+        for (int jj = 15; jj >= 0; --jj) {
+          const int y_hi = t1[16 + jj] - __shfl_sync(0xffffffffu, cown, 16 + jj);
+          const int y_lo = t1[jj] - __shfl_sync(0xffffffffu, cown, jj);
+          wi_hi = __funnelshift_l((uint32_t)(rin1 - y_hi), wi_hi, 1);
+          wi_lo = __funnelshift_l((uint32_t)(rin1 - y_lo), wi_lo, 1);
+          wo_hi = __funnelshift_l((uint32_t)(y_hi - ro1), wo_hi, 1);
+          wo_lo = __funnelshift_l((uint32_t)(y_lo - ro1), wo_lo, 1);
         }
-        ph_acc[0] ^= 1;
-        ph_acc[1] ^= 1;
-        // bitmap words (row, 2 x 32 columns) of tile (I, J)
-        *reinterpret_cast<uint2*>(P.adj + tile * kTileWords + row * 4 + ch * 2) =
-            make_uint2(in_w[0], in_w[1]);
-        if (__any_sync(0xffffffffu, (in_w[0] | in_w[1]) != 0u) && lane == 0)
-          P.nonempty[tile] = 1;
-        row_count += __popc(in_w[0]) + __popc(in_w[1]);
-        // column counts (off-diagonal tiles only): 32x32 bit transposes across
-        // the warp (lane j then holds column j), popc, reduce the 4 row
-        // quarters in smem, one global atomic per column
-        if (J != un.I) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t w = in_w[h];
-            w = bit_transpose_step(w, 16, 0x0000FFFFu, lane);
-            w = bit_transpose_step(w, 8, 0x00FF00FFu, lane);
-            w = bit_transpose_step(w, 4, 0x0F0F0F0Fu, lane);
-            w = bit_transpose_step(w, 2, 0x33333333u, lane);
-            w = bit_transpose_step(w, 1, 0x55555555u, lane);
-            const int my = __popc(w);
-            if (my) atomicAdd(colcnt + cbank * kBN + ch * 64 + h * 32 + lane, my);
-          }
-        }
+        const uint32_t valid = row_ok ? colmask : 0u;
+        const uint32_t iw = (wi_hi << 16) | wi_lo, ow = (wo_hi << 16) | wo_lo;
+        const uint32_t in_w = iw & valid;
+        const uint32_t amb_w = valid & ~iw & ~ow;
+        // bitmap word (row, 32 columns) of the tile
+        P.adj[tile * kTileWords + row * 4 + ch] = in_w;
+        if (__any_sync(0xffffffffu, in_w != 0u) && lane == 0) P.nonempty[tile] = 1;
+        row_count += __popc(in_w);
         EP_MARK(4);
-        epi_bar();
-        EP_MARK(5);
-        if (J != un.I && q == 0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            int32_t* ccp = colcnt + cbank * kBN + ch * 64 + h * 32 + lane;
-            const int v = *ccp;
-            if (v) atomicAdd(P.cnt + pb + col0 + h * 32 + lane, v);
-            *ccp = 0;
-          }
-        }
-        cbank ^= 1;
         // undecided pairs -> exact recheck queue (one atomic per warp)
-        {
-          const int nb0 = __popc(amb_w[0]), nb = nb0 + __popc(amb_w[1]);
+        if (__any_sync(0xffffffffu, amb_w != 0u)) {
+          const int nb = __popc(amb_w);
           int incl = nb;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -672,22 +648,16 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
             if (lane >= o) incl += v;
           }
           const int tot = __shfl_sync(0xffffffffu, incl, 31);
-          if (tot) {
-            unsigned long long base = 0;
-            if (lane == 31) base = atomicAdd(P.qcount, (unsigned long long)tot);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            unsigned long long i = base + (unsigned long long)(incl - nb);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t band = amb_w[h];
-              while (band) {
-                const int j = __ffs(band) - 1;
-                band &= band - 1;
-                if (i < P.qcap)
-                  P.queue[i] = make_int4(pb + gi, pb + col0 + h * 32 + j, (int)tile, k);
-                ++i;
-              }
-            }
+          unsigned long long base = 0;
+          if (lane == 31) base = atomicAdd(P.qcount, (unsigned long long)tot);
+          base = __shfl_sync(0xffffffffu, base, 31);
+          unsigned long long i = base + (unsigned long long)(incl - nb);
+          uint32_t band = amb_w;
+          while (band) {
+            const int j = __ffs(band) - 1;
+            band &= band - 1;
+            if (i < P.qcap) P.queue[i] = make_int4(pb + gi, pb + col0 + j, (int)tile, k);
+            ++i;
           }
         }
         EP_MARK(6);
@@ -1003,6 +973,35 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
   }
 }
 
+// Column counts of the off-diagonal kept tiles of a window (the epilogue takes
+// the row counts): one warp per (tile, 32-column word), 4 row quarters
+// transposed in registers (lane j then holds column j), popc, one atomic per
+// column. Runs before the recheck, which counts the bits it adds itself.
+__global__ void __launch_bounds__(128)
+colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ nonempty,
+                const TileRef* __restrict__ tiles, int64_t slot0, int64_t n_tiles,
+                ElemTables et, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t s = blockIdx.x; s < n_tiles; s += gridDim.x) {
+    if (!nonempty[s]) continue;
+    const TileRef tr = tiles[slot0 + s];
+    if (tr.I == tr.J) continue;
+    const uint32_t* b = adj + s * kTileWords;
+    int acc = 0;
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      uint32_t x = b[(rb * 32 + lane) * 4 + w];
+      x = bit_transpose_step(x, 16, 0x0000FFFFu, lane);
+      x = bit_transpose_step(x, 8, 0x00FF00FFu, lane);
+      x = bit_transpose_step(x, 4, 0x0F0F0F0Fu, lane);
+      x = bit_transpose_step(x, 2, 0x33333333u, lane);
+      x = bit_transpose_step(x, 1, 0x55555555u, lane);
+      acc += __popc(x);
+    }
+    if (acc) atomicAdd(cnt + et.pbase[tr.k] + tr.J * kTile + w * 32 + lane, acc);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // TMA descriptor through the driver entry point (no libcuda link dependency)
 // ---------------------------------------------------------------------------
@@ -1267,6 +1266,9 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
       return BM_ERR_INTERNAL;
     }
   }
+  colcount_kernel<<<grid_cap(n_tiles, 1, 16), 128, 0, stream>>>(adj, nonempty, tiles, slot0,
+                                                                n_tiles, et, cnt_run);
+  BM_CHECK_LAUNCH();
   const int64_t nrec = (int64_t)h_cnt[0];
   if (nrec > 0) {
     const unsigned rg = grid_cap(nrec, kRcWarps * 32, 6);

@@ -9,8 +9,10 @@
  * Conventions
  *   - Every pointer named d_* is DEVICE memory owned by the caller; h_* is
  *     host memory owned by the caller.  The library never returns memory the
- *     caller must free; internal scratch is stream-ordered and released
- *     before the call returns.
+ *     caller must free; internal scratch is stream-ordered (cudaMallocAsync)
+ *     and freed before the call returns, but the device's default pool keeps
+ *     it mapped for the next call (bm_release_scratch trims it;
+ *     B200MAP_POOL_RELEASE=1 disables the retention).
  *   - `stream` is a cudaStream_t (passed as void*); NULL = legacy stream.
  *     Calls that must size outputs synchronise that stream.
  *   - Return value: 0 on success, BM_ERR_DATA (-1) for invalid arguments
@@ -104,10 +106,16 @@ int bm_membership_fill(const double* d_f, int64_t n, int m, const double* h_lo,
  *                 (clusters ordered by smallest row, clustering.py:192-197),
  *                 or -1 for noise;
  *   h_n_clusters[k] number of clusters of element k (synchronises the stream).
- * engine: BM_ENGINE_*.  stats (optional, 8 int64): [0] pairs evaluated,
- * [1] pairs rechecked in exact fp64, [2] tiles skipped, [3] tile pairs total,
- * [4] adjacency bytes, [5] adjacency-stage device time (ns, CUDA events on
- * `stream`), [6] gather/setup time (ns), [7] counts/union-find/relabel time (ns). */
+ * engine: BM_ENGINE_*.  stats (optional, 8 int64): [0] distinct row pairs
+ * inside the computed tile pairs, [1] pairs rechecked in exact fp64,
+ * [2] tile pairs pruned by the centre/radius bound, [3] tile pairs total,
+ * [4] bitmap bytes (largest window), [5] adjacency-stage device time (ns, CUDA
+ * events on `stream`), [6] grouping/gather/quantise/prune time (ns),
+ * [7] core/union-find/relabel time (ns).
+ * Internally rows of an element are regrouped spatially and tile pairs that
+ * provably hold no eps pair are skipped; results do not depend on either
+ * (B200MAP_NO_PRUNE=1 turns both off). An element whose bitmap exceeds the
+ * device budget is processed in row windows (two passes). */
 int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
                         const int64_t* d_rows, const int64_t* h_offsets,
                         int64_t n_el, double eps, int32_t min_pts,

@@ -13,10 +13,14 @@
 // sqrt, compared with eps AFTER the sqrt.
 //
 // Pipeline per batch of elements (see dbscan.cuh for the HBM layout):
-//   gather -> adjacency bitmap (exact fp64 tiles, or tcgen05 candidates +
-//   exact recheck, tc_engine.cu) -> counts -> core -> union-find over
-//   core-core bits (diagonal tiles first, then off-diagonal with global-root
-//   filtering) + border atomicMin -> canonical relabel.
+//   spatial grouping of each element's rows (nearest of 64 chained seeds,
+//   stable sort) -> gather -> tile centres/radii -> pruning of tile pairs
+//   that provably hold no eps pair -> device-built lists of kept tiles and
+//   work units -> adjacency bitmap of the kept tiles (tcgen05 candidates +
+//   exact recheck, tc_engine.cu; or the exact fp64 tile engine) -> counts ->
+//   core -> union-find over core-core bits (diagonal tiles first, then
+//   off-diagonal with empty/uniform-root tiles skipped) + border minima on
+//   entry indices -> canonical relabel on entry indices.
 #include <algorithm>
 #include <vector>
 

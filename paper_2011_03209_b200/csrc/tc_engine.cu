@@ -7,30 +7,44 @@
 // candidate distance must come with a RIGOROUS error bound. Floating-point
 // MMA accumulation has no documented rounding model; integer MMA
 // (kind::i8, s32 accumulate) is exact. Each element is centred (c_k) and
-// quantised to 24-bit fixed point q = rint((x - c_k) / s_k), split into
-// three limbs q = H*2^14 + M*2^7 + L (H signed 8-bit, M/L in [0,127]). The
-// dot product q_i.q_j is the exact sum of 9 limb products; 8 run on the
-// tensor cores (the L.L term, 0 <= LL <= 255^2 d, is bounded instead),
-// accumulated per shift class in 4 TMEM accumulators:
-//   A0 = H.H  A1 = H.M + M.H  A2 = H.L + M.M + L.H  A3 = M.L + L.M
-// D2c = N_i + N_j - 2 (A0<<32 + A1<<24 + A2<<16 + A3<<8) is an exact int64
-// with D2_q in [D2c - 2*LLmax, D2c], where D2_q = |q_i - q_j|^2.
+// quantised to 22-bit fixed point q = rint((x - c_k) / s_k), |q| < 2^21, split
+// into three limbs q = H*2^14 + M*2^7 + L (H signed byte, M, L in [0,127]).
+// Six of the nine limb products run on the tensor cores, accumulated per
+// shift class in three TMEM accumulators (N = 128 columns each):
+//   A0 = H.H   A1 = H.M + M.H   A2 = H.L + M.M + L.H
+// The omitted A3 = M.L + L.M and L.L terms are non-negative and bounded
+// (prm.a3max, prm.ll2), so D2c = N_i + N_j - 2 (A0<<28 + A1<<21 + A2<<14)
+// brackets D2_q = |q_i - q_j|^2 from both sides with known slack.
 // Per point the quantisation error e_i = |x_i - c - s q_i| is measured in
-// fp64; by the triangle inequality |d_true - s sqrt(D2_q)| <= e_i + e_j, and
-// the reference's own fp64 result satisfies |d_ref - d_true| <= gamma d_true.
-// Each 128x64 pair tile gets integer thresholds T_in <= T_out:
-//   D2c <= T_in  -> certainly inside (d_ref <= eps)
-//   D2c >  T_out -> certainly outside
+// fp64 (tile maxima, tile_u); by the triangle inequality
+// |d_true - s sqrt(D2_q)| <= e_i + e_j, and the reference's fp64 result
+// satisfies |d_ref - d_true| <= gamma d_true, gamma = 1.5 (d+16) 2^-53.
+// Each tile pair gets thresholds t_in <= t_out on D2c (tile_thr_kernel):
+//   D2c <= t_in  -> certainly inside (d_ref <= eps)
+//   D2c >  t_out -> certainly outside
 //   otherwise    -> queued and decided by the exact fp64 recheck kernel in
-//                   the element's summation order.
+//                   the element's summation order (~3e-5 of the pairs).
+// In the epilogue one int32 per pair decides: y = 2^7 a0 + a1 + (a2 >> 7)
+// - floor(N_j / 2^22) against per-row integer bounds r_in/r_out (the
+// floors and shifts are absorbed by +-2 margins, see tile_thr_kernel).
 //
-// Kernel: persistent, one CTA per SM, 256 threads. Warp 0 = TMA producer,
-// warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator, warps 4-7 =
-// epilogue (TMEM lanes = rows). A work unit is (element, 128-row tile I,
-// range of 64-row B tiles); the A tile (3 limb planes x Kpad bytes x 128
-// rows, SW128 K-major) stays resident while B tiles stream through a 2-stage
-// TMA ring; accumulators are double-buffered in TMEM (2 x 4 x 64 columns)
-// so the epilogue of tile b overlaps the MMAs of tile b+1.
+// Kernel (tc_adjacency_kernel): persistent, one CTA per SM, 768 threads.
+//   warp 0      TMA producer: per tile the three B limb planes (128 rows x
+//               Kpad bytes each, SWIZZLE_128B 3-D tensor map) into a 2-stage
+//               ring, plus the tile's info (column norms, thresholds, J) by
+//               bulk copy into a 3-deep ring
+//   warp 1      MMA issuer (whole warp, elect.sync): tcgen05.mma.cta_group::1
+//               .kind::i8, M = N = 128, K = 32; accumulator-major order:
+//               phase 1 (A0, A1) then phase 2 (A2), each released separately
+//   warp 2      TMEM allocator (512 columns: A's H/M planes 128 + 3 x 128)
+//   warps 4-19  epilogue: 4 warps per TMEM lane quarter x 32 columns each;
+//               tcgen05.ld -> y -> two sign bits per pair -> bitmap word,
+//               row counts, nonempty flag, undecided pairs to the queue
+//   warps 20-23 A loaders: H/M limb planes of the unit's row tile into TMEM
+//               (tcgen05.st; the MMA reads A from TMEM), L plane by TMA to smem
+// A work unit is (element, 128-row tile I, <= 32 kept column tiles J) over
+// the pruned tile list (dbscan.cu); column counts of off-diagonal tiles come
+// from colcount_kernel, then recheck_kernel decides the queued pairs.
 #include <cuda.h>
 
 #include <stdio.h>

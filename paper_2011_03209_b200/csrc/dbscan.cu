@@ -37,7 +37,9 @@ void tc_release(TcPrep* tp);
 int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
               int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
-              int64_t* stats, cudaStream_t stream);
+              bool sync_check, int64_t* stats, cudaStream_t stream);
+void tc_set_queue_scale(TcPrep* tp, double s);
+int tc_collect(TcPrep* tp, int64_t* rechecked, bool* overflow, cudaStream_t stream);
 
 namespace {
 
@@ -1020,6 +1022,7 @@ struct BatchCtx {
   double eps = 0.0;
   int32_t min_pts = 1;
   bool use_tc = false;
+  double qscale = 1.0;  // recheck queue capacity factor (batch retried on overflow)
   int64_t nb_el = 0, n_tp = 0, P = 0, n_entries = 0, n_rt = 0;
   std::vector<int64_t> tp_off, offs;
   std::vector<int32_t> pbase, nrows, ntiles, tbase;
@@ -1169,7 +1172,10 @@ struct BatchCtx {
     if (prune) BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
     double* cen = prune ? s_geo.as<double>() : nullptr;
     double* rad = prune ? cen + n_rt * d : nullptr;
-    if (use_tc) BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad));
+    if (use_tc) {
+      BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad));
+      tc_set_queue_scale(tc, qscale);
+    }
 
     // ---- kept tile pairs and work units (device-built)
     BM_TRY(build_tiles(d_tbase, prune));
@@ -1223,10 +1229,9 @@ struct BatchCtx {
     BM_TRY(exclusive_scan_i32_to_i64(flags, pos, n_tp, stream));
     fill_total_kernel<<<1, 1, 0, stream>>>(pos, flags, n_tp);  // pos[n_tp] = n_kept
     BM_CHECK_LAUNCH();
-    BM_CHECK_CUDA(cudaMemcpyAsync(&n_kept, pos + n_tp, 8, cudaMemcpyDeviceToHost, stream));
-    BM_CHECK_CUDA(cudaStreamSynchronize(stream));
-    BM_REQUIRE(n_kept < (1ll << 31), "too many tile pairs (%lld)", (long long)n_kept);
-    BM_TRY(scratch_alloc(s_tiles, (size_t)std::max<int64_t>(n_kept, 1) * sizeof(TileRef), stream));
+    // capacity for every tile pair: the list is built before its length is
+    // known on the host (one synchronisation for all row tables below)
+    BM_TRY(scratch_alloc(s_tiles, (size_t)std::max<int64_t>(n_tp, 1) * sizeof(TileRef), stream));
     d_tiles = s_tiles.as<TileRef>();
     // row tables: first slot, pairs, unit positions (exclusive scans)
     BM_TRY(scratch_alloc(s_rows, (size_t)(n_rt + 1) * 8 * 6, stream));
@@ -1255,6 +1260,8 @@ struct BatchCtx {
     BM_CHECK_CUDA(cudaMemcpyAsync(off_pos.data(), d_offp, (n_rt + 1) * 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(tc_pos.data(), d_tcp, (n_rt + 1) * 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+    n_kept = row_first[n_rt];
+    BM_REQUIRE(n_kept < (1ll << 31), "too many tile pairs (%lld)", (long long)n_kept);
     const int64_t n_off_u = off_pos[n_rt], n_tc_u = tc_pos[n_rt];
     BM_TRY(scratch_alloc(s_units, (size_t)(n_rt + n_off_u + n_tc_u + 1) * sizeof(TileUnit), stream));
     d_diag = s_units.as<TileUnit>();
@@ -1306,8 +1313,10 @@ struct BatchCtx {
     BM_TRY(window(I0, I1, w));
     int32_t* nonempty = reinterpret_cast<int32_t*>(adj + w.n_tiles * kTileWords);
     if (use_tc) {
+      // windows (huge elements, row blocks) check the recheck queue at once so
+      // that their counts accumulate exactly once; a whole batch defers it
       BM_TRY(tc_window(tc, xg.as<double>(), et, w.tiles, w.slot0, w.n_tiles, w.tcu, w.n_tc,
-                       w.pairs, adj, nonempty, cnt_acc, I0 >= 0, stats, stream));
+                       w.pairs, adj, nonempty, cnt_acc, I0 >= 0, I0 >= 0, stats, stream));
     } else {
       BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, w.tiles + w.slot0, w.n_tiles, eps,
                                    adj, nonempty, stream));
@@ -1513,47 +1522,68 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
         for (auto p : e) cudaEventDestroy(*p);
       }
     } evg{{&evs, &ev0, &ev1, &ev2}};
-    BM_CHECK_CUDA(cudaEventRecord(evs, stream));
-    BatchCtx bc;
-    bc.stream = stream;
-    bc.d = d;
-    bc.eps = eps;
-    bc.min_pts = min_pts;
-    bc.use_tc = use_tc;
-    BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1, stats));
-    if (bc.n_entries == 0) continue;
-    int32_t* d_out = d_labels + h_offsets[bt.k0];
+    // a batch whose deferred recheck-queue check overflows is rerun with a
+    // larger queue (rare: the capacity is ~10x the typical need)
+    int64_t bst[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool empty = false;
+    for (int attempt = 0;; ++attempt) {
+      for (auto& v : bst) v = 0;
+      BM_CHECK_CUDA(cudaEventRecord(evs, stream));
+      BatchCtx bc;
+      bc.stream = stream;
+      bc.d = d;
+      bc.eps = eps;
+      bc.min_pts = min_pts;
+      bc.use_tc = use_tc;
+      bc.qscale = attempt == 0 ? 1.0 : (attempt == 1 ? 8.0 : 512.0);
+      BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1, bst));
+      if (bc.n_entries == 0) {
+        empty = true;
+        break;
+      }
+      int32_t* d_out = d_labels + h_offsets[bt.k0];
+      std::vector<std::pair<int32_t, int32_t>> wins;
+      if (bt.windowed) {
+        size_t free_now = 0;
+        BM_TRY(device_free_bytes(&free_now));
+        int64_t cap = (int64_t)((0.85 * (double)free_now - (double)(2ll << 30)) /
+                                (kTileWords * 4.0 + kTileAux));
+        if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
+        wins = row_windows(bc, std::max<int64_t>(cap, 1));
+      } else {
+        wins.push_back({-1, -1});
+      }
+      size_t max_w = 0;
+      for (auto& w : wins) max_w = std::max(max_w, bc.window_bytes(w.first, w.second));
+      Scratch adj;
+      BM_TRY(scratch_alloc(adj, max_w, stream));
+      BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
+      // pass 1: counts of every window (the last window's bits stay resident);
+      // pass 2: components of the resident window, then of the others with
+      // their bits recomputed (bit-identical: the decision is a pure function
+      // of the pair)
+      for (auto& w : wins)
+        BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, bst));
+      BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
+      BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
+      for (size_t i = wins.size(); i-- > 0;) {
+        if (i + 1 != wins.size())
+          BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, bst));
+        BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
+      }
+      BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));  // synchronises
+      BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
+      bool overflow = false;
+      if (bc.tc) BM_TRY(tc_collect(bc.tc, &bst[1], &overflow, stream));
+      if (!overflow) break;
+      if (attempt == 2) {
+        set_error("recheck queue overflow");
+        return BM_ERR_INTERNAL;
+      }
+    }
+    if (empty) continue;
+    for (int i = 0; i < 5; ++i) stats[i] = i == 4 ? std::max(stats[4], bst[4]) : stats[i] + bst[i];
     float ms = 0.f, ms_pre = 0.f, ms_post = 0.f;
-    std::vector<std::pair<int32_t, int32_t>> wins;
-    if (bt.windowed) {
-      size_t free_now = 0;
-      BM_TRY(device_free_bytes(&free_now));
-      int64_t cap = (int64_t)((0.85 * (double)free_now - (double)(2ll << 30)) /
-                              (kTileWords * 4.0 + kTileAux));
-      if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
-      wins = row_windows(bc, std::max<int64_t>(cap, 1));
-    } else {
-      wins.push_back({-1, -1});
-    }
-    size_t max_w = 0;
-    for (auto& w : wins) max_w = std::max(max_w, bc.window_bytes(w.first, w.second));
-    Scratch adj;
-    BM_TRY(scratch_alloc(adj, max_w, stream));
-    BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
-    // pass 1: counts of every window (the last window's bits stay resident);
-    // pass 2: components of the resident window, then of the others with
-    // their bits recomputed (bit-identical: the decision is a pure function of
-    // the pair)
-    for (auto& w : wins) BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, stats));
-    BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
-    BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
-    for (size_t i = wins.size(); i-- > 0;) {
-      if (i + 1 != wins.size())
-        BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, stats));
-      BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
-    }
-    BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));
-    BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
     BM_CHECK_CUDA(cudaEventSynchronize(ev2));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     BM_CHECK_CUDA(cudaEventElapsedTime(&ms_pre, evs, ev0));
@@ -1675,6 +1705,10 @@ extern "C" int bm_big_stats(void* handle, int64_t* h_stats) {
   BM_REQUIRE(handle && h_stats, "null argument");
   BigElement* be = static_cast<BigElement*>(handle);
   for (int i = 0; i < 8; ++i) h_stats[i] = be->stats[i];
+  if (be->bc.tc) {
+    bool overflow = false;  // windows check their queue synchronously
+    BM_TRY(tc_collect(be->bc.tc, &h_stats[1], &overflow, be->bc.stream));
+  }
   return BM_OK;
 }
 

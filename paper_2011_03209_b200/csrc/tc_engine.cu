@@ -886,11 +886,13 @@ constexpr int kRcWarps = 4;
 template <int DEPTH>
 __global__ void __launch_bounds__(kRcWarps * 32, 6)
     recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
-                   const int4* __restrict__ queue, int64_t nq, double eps,
+                   const int4* __restrict__ queue, const unsigned long long* __restrict__ nq_ptr,
+                   unsigned long long qcap, double eps,
                    uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
                    int32_t* __restrict__ cnt,
                    unsigned long long* __restrict__ n_inside) {
   __shared__ double sq_all[kRcWarps][32][33];
+  const int64_t nq = (int64_t)(*nq_ptr < qcap ? *nq_ptr : qcap);
   const int lane = threadIdx.x & 31;
   double(*S)[33] = sq_all[threadIdx.x >> 5];
   const int64_t stride = (int64_t)gridDim.x * kRcWarps * 32;
@@ -1069,7 +1071,11 @@ struct TcPrep {
   int nkc = 0, depth = 1;  // depth: pairwise-sum stack depth of d (PwProgram)
   double eps = 0.0;
   std::vector<int32_t> nrows;
-  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw;
+  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw, s_flag;
+  // deferred recheck-queue check: [0] largest overflowing request, [1] pairs
+  // rechecked (device); the caller reads them at its next synchronisation
+  unsigned long long* d_flag = nullptr;
+  double qscale = 1.0;  // recheck queue capacity factor (raised on overflow)
   int32_t* d_tile_elem = nullptr;
   int32_t* d_tbase = nullptr;
   double* tile_u = nullptr;
@@ -1152,14 +1158,36 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
                            stream>>>(tp->s_te.as<unsigned long long>(), tp->d_tile_elem, n_tiles,
                                      scale, n_el, eps, gamma, tp->tile_u, tp->a_in, tp->a_out);
   BM_CHECK_LAUNCH();
-  // the per-point error bounds are folded into tile_u; min/max/centre are
-  // no longer needed
+  BM_TRY(scratch_alloc(tp->s_flag, 16, stream));
+  tp->d_flag = tp->s_flag.as<unsigned long long>();
+  BM_CHECK_CUDA(cudaMemsetAsync(tp->d_flag, 0, 16, stream));
   *out = tp;
   tp = nullptr;  // disarm the guard
   return BM_OK;
 }
 
 void tc_release(TcPrep* tp) { delete tp; }
+
+void tc_set_queue_scale(TcPrep* tp, double s) { tp->qscale = s; }
+
+// after a synchronisation of the stream: pairs rechecked so far and whether a
+// window's recheck queue overflowed (then its bits are incomplete: rerun with
+// a larger tc_set_queue_scale)
+int tc_collect(TcPrep* tp, int64_t* rechecked, bool* overflow, cudaStream_t stream) {
+  unsigned long long h[2] = {0, 0};
+  BM_CHECK_CUDA(cudaMemcpyAsync(h, tp->d_flag, 16, cudaMemcpyDeviceToHost, stream));
+  BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+  *rechecked = (int64_t)h[1];
+  *overflow = h[0] != 0;
+  return BM_OK;
+}
+
+__global__ void queue_check_kernel(const unsigned long long* __restrict__ qcount,
+                                   unsigned long long qcap, unsigned long long* __restrict__ flag) {
+  const unsigned long long c = qcount[0];
+  if (c > qcap) flag[0] = c > flag[0] ? c : flag[0];
+  flag[1] += c < qcap ? c : qcap;
+}
 
 __global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                                   int64_t n) {
@@ -1174,10 +1202,14 @@ __global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __re
 // accumulate: add the window's counts into cnt instead of overwriting it;
 // cnt == nullptr: the counts of this window are not wanted (recomputed window).
 // pairs = distinct row pairs inside the window's tiles (stats and queue size).
+//
+// sync_check: synchronise after the MMA pass and retry it with a larger queue
+// on overflow (counts are accumulated exactly once); otherwise nothing
+// synchronises and an overflow is reported by tc_collect.
 int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
               int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
-              int64_t* stats, cudaStream_t stream) {
+              bool sync_check, int64_t* stats, cudaStream_t stream) {
   const int64_t P = tp->P, d = tp->d;
   const int nkc = tp->nkc;
   if (n_units == 0) return BM_OK;
@@ -1189,8 +1221,10 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   }
 
   // ---- MMA pass (re-run with a larger recheck queue on overflow)
-  unsigned long long qcap =
-      std::max<unsigned long long>(1ull << 20, (unsigned long long)(pairs / 2000));
+  unsigned long long qcap = std::max<unsigned long long>(
+      1ull << 20, (unsigned long long)(tp->qscale * (double)pairs / 2000.0));
+  static const char* force_q = getenv("B200MAP_TEST_QCAP");  // tests: tiny queue
+  if (force_q) qcap = (unsigned long long)(tp->qscale * (double)atoll(force_q));
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
   const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;
@@ -1252,6 +1286,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     else
       tc_adjacency_kernel<2><<<grid, kThreads, smem, stream>>>(tp->qmap, prm);
     BM_CHECK_LAUNCH();
+    if (!sync_check && !tc_prof) break;
     BM_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
     if (tc_prof) {
@@ -1273,7 +1308,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
               100 * e[4] / e[7], 100 * e[5] / e[7], 100 * e[6] / e[7],
               100 * (e[7] - e[0] - e[1] - e[2] - e[3] - e[4] - e[5] - e[6]) / e[7]);
     }
-    if (h_cnt[0] <= qcap) break;
+    if (h_cnt[0] <= qcap || !sync_check) break;
     qcap = h_cnt[0] + 1024;
     if (attempt == 2) {
       set_error("recheck queue overflow");
@@ -1283,24 +1318,27 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   colcount_kernel<<<grid_cap(n_tiles, 1, 16), 128, 0, stream>>>(adj, nonempty, tiles, slot0,
                                                                 n_tiles, et, cnt_run);
   BM_CHECK_LAUNCH();
-  const int64_t nrec = (int64_t)h_cnt[0];
-  if (nrec > 0) {
-    const unsigned rg = grid_cap(nrec, kRcWarps * 32, 6);
+  {
+    // the queue length stays on the device: the recheck grid covers the
+    // capacity and each warp reads the count
+    const unsigned rg = grid_cap((int64_t)qcap, kRcWarps * 32, 6);
     const int4* q = s_q.as<int4>();
     switch (tp->depth) {
       case 1:
-        recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
-                                                            nonempty, cnt_run, d_cnt + 1);
+        recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+                                                            adj, nonempty, cnt_run, d_cnt + 1);
         break;
       case 2:
-        recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
-                                                            nonempty, cnt_run, d_cnt + 1);
+        recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+                                                            adj, nonempty, cnt_run, d_cnt + 1);
         break;
       default:
-        recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, nrec, tp->eps, adj,
-                                                            nonempty, cnt_run, d_cnt + 1);
+        recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+                                                            adj, nonempty, cnt_run, d_cnt + 1);
         break;
     }
+    BM_CHECK_LAUNCH();
+    queue_check_kernel<<<1, 1, 0, stream>>>(d_cnt, qcap, tp->d_flag);
     BM_CHECK_LAUNCH();
   }
   if (accumulate && cnt) {
@@ -1308,7 +1346,6 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     BM_CHECK_LAUNCH();
   }
   stats[0] += pairs;
-  stats[1] += nrec;
   return BM_OK;
 }
 

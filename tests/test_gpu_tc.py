@@ -1,6 +1,8 @@
 """GPU: the tensor-core (tcgen05 kind::i8) adjacency engine decides every eps
 pair exactly like the fp64 engine (and hence like the reference)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -72,3 +74,36 @@ def test_tc_large_offsets_and_nan():
     b, nb, _ = labels(X, [rows], eps, 3, [0], 2)
     assert np.array_equal(a, b) and np.array_equal(na, nb)
     assert a[17] == -1  # NaN point is in no neighbourhood (sqrt(NaN) <= eps is False)
+
+
+@pytest.mark.parametrize("qcap", ["40", "3"])
+def test_recheck_queue_overflow_reruns(qcap):
+    """A recheck queue too small for the undecided pairs is detected after the
+    batch (no synchronisation inside it) and the batch reruns with a larger
+    queue; windows (sync-checked) retry in place. Results are unchanged."""
+    import subprocess
+    import sys
+
+    code = f"""
+import os, sys, numpy as np
+sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
+from test_gpu_tc import labels
+from oracle import mapper_oracle as O
+X = O.gmm(3000, 128, 4, 3.0, 5)
+eps = O.dist_quantile(X, 0.05, 5)
+rows = np.arange(3000)
+lab, ncl, st = labels(X, [rows], eps, 5, [O.ORDER_SEQUENTIAL], 2)
+clusters, noise = O.dbscan_element(X, rows, eps, 5, O.ORDER_SEQUENTIAL)
+got = [rows[lab == c].tolist() for c in range(int(ncl[0]))]
+assert got == clusters and rows[lab < 0].tolist() == noise
+print("rechecks", st[1])
+"""
+    for window in (None, "3"):
+        env = dict(os.environ, B200MAP_TEST_QCAP=qcap)
+        if window:
+            env["B200MAP_WINDOW_TILES"] = window
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert int(r.stdout.split()[-1]) > int(qcap)  # the queue did overflow

@@ -5,6 +5,9 @@
 #include <atomic>
 #include <mutex>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace bm {
@@ -45,6 +48,46 @@ static void retain_pool_once() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   cudaGetLastError();
+}
+
+namespace {
+struct TraceMark {
+  const char* name;
+  double host_ms;
+  cudaEvent_t ev;
+};
+std::vector<TraceMark>& trace_marks() {
+  static thread_local std::vector<TraceMark> m;
+  return m;
+}
+bool trace_on() {
+  static const bool on = getenv("B200MAP_TRACE") != nullptr;
+  return on;
+}
+}  // namespace
+
+void trace_mark(const char* name, cudaStream_t s) {
+  if (!trace_on()) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  TraceMark m{name, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), nullptr};
+  cudaEventCreate(&m.ev);
+  cudaEventRecord(m.ev, s);
+  trace_marks().push_back(m);
+}
+
+void trace_dump() {
+  if (!trace_on()) return;
+  auto& m = trace_marks();
+  if (m.empty()) return;
+  cudaEventSynchronize(m.back().ev);
+  fprintf(stderr, "[trace] %-28s %10s %10s\n", "mark", "host ms", "device ms");
+  for (auto& x : m) {
+    float dev = 0.f;
+    cudaEventElapsedTime(&dev, m.front().ev, x.ev);
+    fprintf(stderr, "[trace] %-28s %10.3f %10.3f\n", x.name, x.host_ms - m.front().host_ms, dev);
+  }
+  for (auto& x : m) cudaEventDestroy(x.ev);
+  m.clear();
 }
 
 int device_free_bytes(size_t* free_b) {

@@ -81,6 +81,11 @@ int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream);
 // graph.cu); result in place. vals may be null.
 int sort_pairs_u64(uint64_t* keys, int64_t* vals, int64_t n, int key_bits, cudaStream_t s);
 
+// Dev tracing (B200MAP_TRACE=1): host time and a device event per mark;
+// trace_dump() (after a synchronisation) prints both timelines.
+void trace_mark(const char* name, cudaStream_t s);
+void trace_dump();
+
 // Free device memory including what the stream-ordered pool retains unused.
 int device_free_bytes(size_t* free_b);
 

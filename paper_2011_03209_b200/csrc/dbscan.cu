@@ -1099,6 +1099,7 @@ struct BatchCtx {
     const int64_t* rows_b = d_rows + h_offsets[k0];
     const bool prune = prune_enabled(d);
 
+    trace_mark("setup:tables", stream);
     // ---- row order inside each element: grouped (stable by seed) or identity
     {
       Scratch s_k, s_v, s_it;
@@ -1148,6 +1149,7 @@ struct BatchCtx {
       BM_CHECK_LAUNCH();
     }
 
+    trace_mark("setup:grouped", stream);
     // ---- gather rows (fp64, padded order)
     BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
     gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
@@ -1172,13 +1174,16 @@ struct BatchCtx {
     if (prune) BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
     double* cen = prune ? s_geo.as<double>() : nullptr;
     double* rad = prune ? cen + n_rt * d : nullptr;
+    trace_mark("setup:gathered", stream);
     if (use_tc) {
       BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad));
       tc_set_queue_scale(tc, qscale);
     }
 
     // ---- kept tile pairs and work units (device-built)
+    trace_mark("setup:quantised", stream);
     BM_TRY(build_tiles(d_tbase, prune));
+    trace_mark("setup:tiles", stream);
     s_geo.release();
     stats[3] += n_tp;
     stats[2] += n_tp - n_kept;
@@ -1442,6 +1447,7 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
                                    const uint8_t* h_order, int engine, int32_t* d_labels,
                                    int32_t* h_n_clusters, int64_t* h_stats, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
+  trace_mark("cluster:entry", stream);
   BM_REQUIRE(n >= 0 && d >= 1 && n_el >= 0, "bad shapes");
   BM_REQUIRE(eps > 0.0, "eps must be positive");
   BM_REQUIRE(min_pts >= 1, "min-pts must be >= 1");
@@ -1529,6 +1535,7 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     for (int attempt = 0;; ++attempt) {
       for (auto& v : bst) v = 0;
       BM_CHECK_CUDA(cudaEventRecord(evs, stream));
+      trace_mark("batch:start", stream);
       BatchCtx bc;
       bc.stream = stream;
       bc.d = d;
@@ -1564,6 +1571,7 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       // of the pair)
       for (auto& w : wins)
         BM_TRY(bc.adjacency(w.first, w.second, adj.as<uint32_t>(), bc.cnt, bst));
+      trace_mark("adjacency", stream);
       BM_CHECK_CUDA(cudaEventRecord(ev1, stream));
       BM_TRY(bc.init_core(bc.cnt, bc.par, bc.bmin));
       for (size_t i = wins.size(); i-- > 0;) {
@@ -1571,7 +1579,9 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
           BM_TRY(bc.adjacency(wins[i].first, wins[i].second, adj.as<uint32_t>(), nullptr, bst));
         BM_TRY(bc.components(wins[i].first, wins[i].second, adj.as<uint32_t>(), bc.par, bc.bmin));
       }
+      trace_mark("components", stream);
       BM_TRY(bc.finish(bc.par, bc.bmin, d_out, h_n_clusters + bt.k0));  // synchronises
+      trace_mark("finished", stream);
       BM_CHECK_CUDA(cudaEventRecord(ev2, stream));
       bool overflow = false;
       if (bc.tc) BM_TRY(tc_collect(bc.tc, &bst[1], &overflow, stream));
@@ -1592,6 +1602,8 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
     stats[6] += (int64_t)(ms_pre * 1e6);   // grouping, gather, quantisation, pruning
     stats[7] += (int64_t)(ms_post * 1e6);  // core, union-find, border, relabel (+ recomputed windows)
   }
+  trace_mark("cluster:return", stream);
+  trace_dump();
   return BM_OK;
 }
 

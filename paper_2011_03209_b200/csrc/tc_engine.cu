@@ -1135,6 +1135,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   BM_TRY(scratch_alloc(tp->s_te, (size_t)n_tiles * 8, stream));
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_te.ptr, 0, n_tiles * 8, stream));
 
+  trace_mark("tc:prep start", stream);
   tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, tp->d_tile_elem, n_tiles,
                                                             tmin, tmax, cen);
   BM_CHECK_LAUNCH();
@@ -1286,6 +1287,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     else
       tc_adjacency_kernel<2><<<grid, kThreads, smem, stream>>>(tp->qmap, prm);
     BM_CHECK_LAUNCH();
+    trace_mark("tc:mma launched", stream);
     if (!sync_check && !tc_prof) break;
     BM_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 8, cudaMemcpyDeviceToHost, stream));
     BM_CHECK_CUDA(cudaStreamSynchronize(stream));
@@ -1340,6 +1342,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     BM_CHECK_LAUNCH();
     queue_check_kernel<<<1, 1, 0, stream>>>(d_cnt, qcap, tp->d_flag);
     BM_CHECK_LAUNCH();
+    trace_mark("tc:recheck launched", stream);
   }
   if (accumulate && cnt) {
     add_counts_kernel<<<grid_cap(P, 256, 8), 256, 0, stream>>>(cnt, cnt_run, P);

@@ -201,15 +201,15 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
 
     from . import engine as eng
     from .clustering import DbscanParams, cluster_device, effective_mem_budget, element_orders
-    from .cover import build_cover
-    from .filters import FilterValues, evaluate_device
+    from .cover import build_cover_from_range
+    from .filters import evaluate_device
     from .pipeline import DeviceGraph
 
     cols = [evaluate_device(X, pc, s) for s in params.filters]
     F = torch.stack(cols, dim=1).contiguous() if len(cols) > 1 else cols[0].reshape(-1, 1)
-    fv_host = F.cpu().numpy()
-    cover = build_cover(FilterValues(values=fv_host.copy(), specs=list(params.filters)),
-                        params.n, params.p)
+    rng = torch.stack([F.amin(dim=0), F.amax(dim=0)], dim=1).cpu().numpy()
+    cover = build_cover_from_range([(rng[a, 0], rng[a, 1]) for a in range(F.shape[1])],
+                                   params.n, params.p)
     rows, offsets = eng.membership(F, cover)
     sizes = np.diff(offsets)
     budget = effective_mem_budget() if budget_bytes is None else budget_bytes
@@ -244,6 +244,6 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     node_rows, node_off, n_nodes = eng.group_nodes(rows, offsets, labels, ncl)
     node_elem = np.repeat(np.arange(len(ncl)), ncl)
     edges = eng.nerve_edges(node_rows, node_off, n_nodes, X.shape[0])
-    return DeviceGraph(F=F, fv_host=fv_host, cover=cover, sizes=sizes, orders=orders,
+    return DeviceGraph(F=F, cover=cover, sizes=sizes, orders=orders,
                        node_rows=node_rows, node_off=node_off, node_elem=node_elem,
                        n_nodes=n_nodes, edges=edges, dev_stats=st, timings={}), st

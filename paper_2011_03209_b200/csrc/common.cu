@@ -134,6 +134,22 @@ int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
   return BM_OK;
 }
 
+size_t device_total_bytes() {
+  static std::mutex mu;
+  static size_t cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && cache[dev]) return cache[dev];
+  size_t f = 0, t = 0;
+  if (cudaMemGetInfo(&f, &t) != cudaSuccess) {
+    cudaGetLastError();
+    t = 0;
+  }
+  if (dev < 64) cache[dev] = t;
+  return t;
+}
+
 int num_sms() {
   static std::mutex mu;
   static int cache[64] = {0};

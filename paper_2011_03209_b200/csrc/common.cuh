@@ -93,6 +93,8 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Number of SMs on the current device (cached per device).
 int num_sms();
+// Total memory of the current device (cached per device).
+size_t device_total_bytes();
 
 // ---------------------------------------------------------------------------
 // Device-wide exclusive scan over int64 (in-place allowed). n may be 0.

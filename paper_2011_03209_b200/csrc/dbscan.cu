@@ -1481,10 +1481,18 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
   // ---- batches bounded by the device budget (dense bitmap estimate); an
   //      element whose dense bitmap alone exceeds it is processed by itself in
   //      row windows sized on its kept tiles
-  size_t free_b = 0;
-  BM_TRY(device_free_bytes(&free_b));
-  const double budget = 0.55 * (double)free_b;
+  // free memory is queried only when the work could come near it: the query
+  // (cudaMemGetInfo + pool attributes) intermittently stalls for tens of ms
   const int64_t forced_cap = row_window_cap();
+  double need = 0.0;
+  for (int64_t k = 0; k < n_el; ++k) {
+    const int64_t T = ceil_div(h_offsets[k + 1] - h_offsets[k], kTile);
+    need += (double)(T * (T + 1) / 2) * (kTileWords * 4 + kTileAux) +
+            (double)T * kTile * (d * 8.0 + 4 * 9 + 1 + 24 + d * 3.0);
+  }
+  size_t free_b = device_total_bytes();
+  if (need > 0.2 * (double)free_b || forced_cap > 0) BM_TRY(device_free_bytes(&free_b));
+  const double budget = 0.55 * (double)free_b;
   struct Batch {
     int64_t k0, k1;
     bool windowed;  // single huge element in row windows

@@ -120,6 +120,22 @@ def alg_flops(sizes, d):
     return float((2.0 * d * s * (s - 1) / 2.0).sum())
 
 
+def ncu_traffic(kernel="tc_adjacency_kernel"):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/r01_ncu_full_cfg3.txt)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_cfg3.txt")) as f:
+            block = None
+            for line in f:
+                if line.startswith("void ") or line.startswith("unnamed"):
+                    block = line
+                if block and kernel in block and "dram traffic" in line:
+                    return float(line.split()[-1])
+    except OSError:
+        pass
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -342,7 +358,9 @@ def main():
         "e2e": {"value": w.n * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic(),
+                     "traffic_note": "DRAM bytes per tc_adjacency_kernel launch, ncu --set full "
+                                     "(profiles/r01_ncu_full_cfg3.txt)",
                      "kernel": "eps-adjacency (distance tiles) stage",
                      "kernel_ms_per_step": adj_s * 1e3,
                      "kernel_share_of_step": adj_s / (t_dev / args.steps),

@@ -74,7 +74,7 @@ __global__ void gather_kernel(const double* __restrict__ X, int64_t d,
 // tiles compact, so tile pairs of far-apart groups can be pruned.
 // ---------------------------------------------------------------------------
 constexpr int kGroupSeeds = 64;
-constexpr int kGroupDims = 64;
+constexpr int kGroupDims = 32;
 constexpr int kGroupMinRows = 3 * kTile;  // smaller elements keep their order
 
 struct GroupItem {

@@ -88,7 +88,7 @@ struct GroupItem {
 __global__ void __launch_bounds__(256)
 seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                   const int64_t* __restrict__ offs, const int32_t* __restrict__ elems,
-                  int32_t* __restrict__ rank) {
+                  int32_t* __restrict__ rank, int32_t* __restrict__ order) {
   __shared__ float sd[kGroupSeeds][kGroupDims + 1];
   __shared__ float dist[kGroupSeeds][kGroupSeeds + 1];
   __shared__ int used[kGroupSeeds];
@@ -117,6 +117,7 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
     int cur = 0;
     if (lane == 0) {
       rank[(int64_t)k * kGroupSeeds] = 0;
+      for (int r = 0; r < kGroupSeeds; ++r) order[(int64_t)k * kGroupSeeds + r] = r ? -1 : 0;
       used[0] = 1;
     }
     __syncwarp();
@@ -139,6 +140,7 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
       cur = bi;
       if (lane == 0) {
         rank[(int64_t)k * kGroupSeeds + cur] = step;
+        order[(int64_t)k * kGroupSeeds + step] = cur;
         used[cur] = 1;
       }
       __syncwarp();
@@ -241,6 +243,190 @@ __global__ void perm_kernel(const int64_t* __restrict__ sorted, const int64_t* _
 }
 
 // ---------------------------------------------------------------------------
+// Direction bound (second pruning test). Every grouped element keeps its 64
+// seed points s_g (full d, fp64). Row tile T is labelled with the seed a of
+// its middle row; for every seed g the kernel below stores
+//   proj_T[g] <= min_{x in T} <x, s_a - s_g>
+// (fp32 dot products, minus a rigorous bound of their rounding). For tiles I
+// (seed a) and J (seed b != a), u = s_a - s_b gives for all x in I, y in J
+//   |x - y| >= <x - y, u>/|u| = (<x,u> + <y,-u>)/|u| >= (proj_I[b] + proj_J[a]) / |u|,
+// which prunes most tile pairs of different seed groups that the centre/radius
+// bound cannot (the groups are far apart along u, wide across it).
+// ---------------------------------------------------------------------------
+// per row tile: its seed (-1: element not grouped)
+__global__ void tile_seed_kernel(ElemTables et, const int64_t* __restrict__ offs, int64_t n_rt,
+                                 const uint64_t* __restrict__ skeys,
+                                 const int32_t* __restrict__ order, int64_t min_rows,
+                                 int32_t* __restrict__ tseed) {
+  for (int64_t rt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rt < n_rt;
+       rt += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = rt * kTile;
+    int64_t a = 0, b = et.n_el;
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (et.pbase[mid] <= p0) a = mid; else b = mid;
+    }
+    const int k = (int)a;
+    int seed = -1;
+    if (et.nrows[k] >= min_rows) {
+      const int64_t i0 = p0 - et.pbase[k];
+      const int64_t valid = min((int64_t)kTile, (int64_t)et.nrows[k] - i0);
+      const uint64_t key = skeys[offs[k] + i0 + valid / 2];
+      seed = order[(int64_t)k * kGroupSeeds + (int)(key & 127)];
+    }
+    tseed[rt] = seed;
+  }
+}
+
+// per (grouped element, seed a) (one CTA): fp32 copy and fp64 norm of seed a,
+// fp64 distances from seed a to every seed (one warp per seed b)
+__global__ void __launch_bounds__(256)
+seed_data_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                 const int64_t* __restrict__ offs, const int32_t* __restrict__ elems,
+                 float* __restrict__ sf, double* __restrict__ snorm,
+                 double* __restrict__ sdist) {
+  const int k = elems[blockIdx.x / kGroupSeeds];
+  const int ga = blockIdx.x % kGroupSeeds;
+  const int64_t ek = offs[k], nk = offs[k + 1] - ek;
+  const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
+  float* sfa = sf + ((int64_t)k * kGroupSeeds + ga) * d;
+  const double* xa = ga < S ? X + rows[ek + (ga * nk) / S] * d : nullptr;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) sfa[c] = xa ? (float)xa[c] : 0.0f;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int gb = w; gb < kGroupSeeds; gb += blockDim.x >> 5) {
+    double acc = 0.0, na = 0.0;
+    if (xa && gb < S) {
+      const double* xb = X + rows[ek + (gb * nk) / S] * d;
+      for (int64_t c = lane; c < d; c += 32) {
+        const double df = xa[c] - xb[c];
+        acc = fma(df, df, acc);
+        if (gb == 0) na = fma(xa[c], xa[c], na);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+    }
+    if (lane == 0) {
+      sdist[((int64_t)k * kGroupSeeds + ga) * kGroupSeeds + gb] = sqrt(acc);
+      if (gb == 0) snorm[(int64_t)k * kGroupSeeds + ga] = sqrt(na);
+    }
+  }
+}
+
+constexpr int kProjKC = 16;  // dims staged per step (register-prefetched)
+
+// one CTA per grouped row tile: D[x][g] = <x, s_g> for its 128 rows and the 64
+// seeds (fp32, 4 x 8 per thread), then proj[rt][g] = min_x (D[x][a] - D[x][g])
+// minus the rounding bound (d + 2) 2^-23 (|c_T| + r_T)(|s_a| + |s_g|)
+__global__ void __launch_bounds__(256, 3)
+tile_project_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, int64_t n_rt,
+                    const int32_t* __restrict__ tseed, const float* __restrict__ sf,
+                    const double* __restrict__ snorm, const double* __restrict__ cen,
+                    const double* __restrict__ rad, double* __restrict__ proj) {
+  // staging (xs, ss) during the dot products; the dot matrix dd afterwards
+  constexpr int kStage = kProjKC * (kTile + 4) + kProjKC * (kGroupSeeds + 4);
+  constexpr int kDot = kTile * (kGroupSeeds + 1);
+  __shared__ __align__(16) float sbuf[kStage > kDot ? kStage : kDot];
+  float(*xs)[kTile + 4] = reinterpret_cast<float(*)[kTile + 4]>(sbuf);
+  float(*ss)[kGroupSeeds + 4] =
+      reinterpret_cast<float(*)[kGroupSeeds + 4]>(sbuf + kProjKC * (kTile + 4));
+  float(*dd)[kGroupSeeds + 1] = reinterpret_cast<float(*)[kGroupSeeds + 1]>(sbuf);
+  __shared__ double cn;
+  const int64_t rt = blockIdx.x;
+  const int a = tseed[rt];
+  if (a < 0) return;  // block-uniform
+  const int64_t p0 = rt * kTile;
+  int64_t lo = 0, hi = et.n_el;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (et.pbase[mid] <= p0) lo = mid; else hi = mid;
+  }
+  const int k = (int)lo;
+  const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
+  const float* sfk = sf + (int64_t)k * kGroupSeeds * d;
+  const int t = threadIdx.x, ty = t >> 3, tx = t & 7;  // points 4ty.., seeds 8tx..
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+  // each thread stages 8 row values and 4 seed values per step; the next
+  // step's values are loaded into registers while the current one computes
+  constexpr int kXv = kTile * kProjKC / 256, kSv = kGroupSeeds * kProjKC / 256;
+  double xr[kXv];
+  float sr[kSv];
+  auto fetch = [&](int64_t c0) {
+#pragma unroll
+    for (int u = 0; u < kXv; ++u) {
+      const int i = t + u * 256, pnt = i / kProjKC, c = i % kProjKC;
+      xr[u] = (c0 + c < d && pnt < valid) ? Xg[(p0 + pnt) * d + c0 + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kSv; ++u) {
+      const int i = t + u * 256, g = i / kProjKC, c = i % kProjKC;
+      sr[u] = c0 + c < d ? sfk[(int64_t)g * d + c0 + c] : 0.0f;
+    }
+  };
+  auto stage = [&]() {
+#pragma unroll
+    for (int u = 0; u < kXv; ++u) {
+      const int i = t + u * 256;
+      xs[i % kProjKC][i / kProjKC] = (float)xr[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kSv; ++u) {
+      const int i = t + u * 256;
+      ss[i % kProjKC][i / kProjKC] = sr[u];
+    }
+  };
+  fetch(0);
+  for (int64_t c0 = 0; c0 < d; c0 += kProjKC) {
+    __syncthreads();
+    stage();
+    __syncthreads();
+    if (c0 + kProjKC < d) fetch(c0 + kProjKC);
+#pragma unroll
+    for (int c = 0; c < kProjKC; ++c) {
+      const float4 xa = *reinterpret_cast<const float4*>(&xs[c][4 * ty]);
+      const float4 s0 = *reinterpret_cast<const float4*>(&ss[c][8 * tx]);
+      const float4 s1 = *reinterpret_cast<const float4*>(&ss[c][8 * tx + 4]);
+      const float xv[4] = {xa.x, xa.y, xa.z, xa.w};
+      const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xv[i], sv[j], acc[i][j]);
+    }
+  }
+  __syncthreads();  // staging buffers are reused for dd
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dd[4 * ty + i][8 * tx + j] = acc[i][j];
+  if (t < 32) {  // |c_T| (fp64)
+    double q = 0.0;
+    for (int64_t c = t; c < d; c += 32) q = fma(cen[rt * d + c], cen[rt * d + c], q);
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (t == 0) cn = sqrt(q);
+  }
+  __syncthreads();
+  if (t < kGroupSeeds) {
+    float m = 3.0e38f;
+    for (int pnt = 0; pnt < valid; ++pnt) m = fminf(m, dd[pnt][a] - dd[pnt][t]);
+    // |fl(<x,s>) - <x,s>| <= (d+2) 2^-24 |x||s| for the fp32 inputs and FMA
+    // chain; doubled for the input rounding of x and s, and the difference of
+    // two dots is rounded once more (absorbed by the +2)
+    const double xmax = (cn + rad[rt]) * (1.0 + 1e-12);
+    const double err = ((double)d + 4.0) * 1.1920928955078125e-07 * xmax *
+                       (snorm[(int64_t)k * kGroupSeeds + a] + snorm[(int64_t)k * kGroupSeeds + t]) *
+                       (1.0 + 1e-9);
+    const double v = (double)m - err;
+    proj[rt * kGroupSeeds + t] = (m == m && rad[rt] == rad[rt]) ? v : -1.0e300;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Tile geometry and pruning. Per 128-row tile: a centre c (the fp64 mean of
 // its rows — any point works) and a radius r >= max |x - c| (fp64 norm plus
 // a relative margin far above its rounding error). For I != J, every pair of
@@ -304,7 +490,8 @@ __global__ void __launch_bounds__(256)
 tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
                   const PruneBlock* __restrict__ blocks, const double* __restrict__ cen,
                   const double* __restrict__ rad, double eps, double gamma,
-                  int32_t* __restrict__ flags) {
+                  const int32_t* __restrict__ tseed, const double* __restrict__ proj,
+                  const double* __restrict__ sdist, int32_t* __restrict__ flags) {
   __shared__ double sa[kPruneDC][kPruneB + 1], sb[kPruneDC][kPruneB + 1];
   const PruneBlock pbk = blocks[blockIdx.x];
   const int k = pbk.k, T = et.ntiles[k];
@@ -353,6 +540,14 @@ tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
         const double rsum = (rad[tb + I] + rad[tb + J]) * (1.0 + 1e-12) + 1e-300;
         const double lb = (sqrt(acc[a][b]) * (1.0 - 1e-12) - rsum) * (1.0 - gamma);
         keep = lb > eps ? 0 : 1;
+        if (keep && tseed) {  // direction bound between the tiles' seed groups
+          const int sa = tseed[tb + I], sb = tseed[tb + J];
+          if (sa >= 0 && sb >= 0 && sa != sb) {
+            const double u = sdist[((int64_t)k * kGroupSeeds + sa) * kGroupSeeds + sb];
+            const double num = proj[(tb + I) * kGroupSeeds + sb] + proj[(tb + J) * kGroupSeeds + sa];
+            if (u > 0.0 && num > 0.0 && (num / (u * (1.0 + 1e-12))) * (1.0 - gamma) > eps) keep = 0;
+          }
+        }
       }
       flags[et.tp_off[k] + tri_index(I, J, T)] = keep;
     }
@@ -1032,7 +1227,12 @@ struct BatchCtx {
   // n_kept), first off-diagonal / tensor-core unit (n_rt+1), row pairs
   int64_t n_kept = 0;
   std::vector<int64_t> row_first, off_pos, tc_pos, row_pairs;
-  Scratch tabs, xg, work, perm, s_tiles, s_units, s_geo;
+  Scratch tabs, xg, work, perm, s_tiles, s_units, s_geo, s_dir, s_seed;
+  // direction bound: per row tile its seed (s_dir), per grouped element the
+  // seeds (fp32), their norms and pairwise distances (s_seed); null if none
+  int32_t* tseed = nullptr;
+  float* seed_f = nullptr;
+  double *seed_norm = nullptr, *seed_dist = nullptr;
   TileRef* d_tiles = nullptr;
   TileUnit *d_diag = nullptr, *d_off = nullptr, *d_tcu = nullptr;
   ElemTables et{};
@@ -1126,12 +1326,22 @@ struct BatchCtx {
         for (int64_t i = 0; i < nb_el; ++i)
           if (nrows[i] >= min_rows) gel.push_back((int32_t)i);
         Scratch s_rank, s_gel;
-        BM_TRY(scratch_alloc(s_rank, (size_t)nb_el * kGroupSeeds * 4, stream));
+        BM_TRY(scratch_alloc(s_rank, (size_t)nb_el * kGroupSeeds * 4 * 2, stream));
         BM_TRY(scratch_alloc(s_gel, gel.size() * 4, stream));
         BM_CHECK_CUDA(cudaMemcpyAsync(s_gel.ptr, gel.data(), gel.size() * 4,
                                       cudaMemcpyHostToDevice, stream));
+        int32_t* d_order = s_rank.as<int32_t>() + nb_el * kGroupSeeds;
         seed_order_kernel<<<(unsigned)gel.size(), 256, 0, stream>>>(
-            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>());
+            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>(), d_order);
+        BM_CHECK_LAUNCH();
+        // seeds for the direction bound (fp32 copy, norms, pair distances)
+        BM_TRY(scratch_alloc(s_seed, (size_t)nb_el * kGroupSeeds * (d * 4 + 8 + kGroupSeeds * 8),
+                             stream));
+        seed_norm = s_seed.as<double>();
+        seed_dist = seed_norm + nb_el * kGroupSeeds;
+        seed_f = reinterpret_cast<float*>(seed_dist + (int64_t)nb_el * kGroupSeeds * kGroupSeeds);
+        seed_data_kernel<<<(unsigned)(gel.size() * kGroupSeeds), 256, 0, stream>>>(
+            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), seed_f, seed_norm, seed_dist);
         BM_CHECK_LAUNCH();
         BM_TRY(scratch_alloc(s_it, items.size() * sizeof(GroupItem), stream));
         BM_CHECK_CUDA(cudaMemcpyAsync(s_it.ptr, items.data(), items.size() * sizeof(GroupItem),
@@ -1143,6 +1353,11 @@ struct BatchCtx {
         int bits = 7;
         while (bits < 64 && ((uint64_t)nb_el << 7) >> bits) ++bits;
         BM_TRY(sort_pairs_u64(s_k.as<uint64_t>(), s_v.as<int64_t>(), n_entries, bits, stream));
+        BM_TRY(scratch_alloc(s_dir, (size_t)n_rt * 4, stream));
+        tseed = s_dir.as<int32_t>();
+        tile_seed_kernel<<<grid_for(n_rt, 256), 256, 0, stream>>>(
+            et, d_offs, n_rt, s_k.as<uint64_t>(), d_order, min_rows, tseed);
+        BM_CHECK_LAUNCH();
       }
       perm_kernel<<<grid_for(P, 256), 256, 0, stream>>>(s_v.as<int64_t>(), d_offs, et, P, ent,
                                                         inv);
@@ -1218,11 +1433,20 @@ struct BatchCtx {
       BM_CHECK_CUDA(cudaMemcpyAsync(s_blk.ptr, blocks.data(), nblk * sizeof(PruneBlock),
                                     cudaMemcpyHostToDevice, stream));
       const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;
+      Scratch s_proj;
+      double* proj = nullptr;
+      if (tseed) {
+        BM_TRY(scratch_alloc(s_proj, (size_t)n_rt * kGroupSeeds * 8, stream));
+        proj = s_proj.as<double>();
+        tile_project_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
+            xg.as<double>(), d, et, n_rt, tseed, seed_f, seed_norm, cen, rad, proj);
+        BM_CHECK_LAUNCH();
+      }
       for (int64_t b0 = 0; b0 < nblk; b0 += (1ll << 30)) {
         const int64_t nb = std::min<int64_t>(1ll << 30, nblk - b0);
-        tile_prune_kernel<<<(unsigned)nb, 256, 0, stream>>>(et, d, d_tbase,
-                                                            s_blk.as<PruneBlock>() + b0, cen, rad,
-                                                            eps, gamma, flags);
+        tile_prune_kernel<<<(unsigned)nb, 256, 0, stream>>>(
+            et, d, d_tbase, s_blk.as<PruneBlock>() + b0, cen, rad, eps, gamma, tseed, proj,
+            seed_dist, flags);
         BM_CHECK_LAUNCH();
       }
     } else {

@@ -183,6 +183,26 @@ int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_offsets,
                    int64_t n_nodes, int64_t n_points, int64_t* d_edges,
                    int64_t* h_n_edges, void* stream);
 
+/* ---- canonical JSON of the node array (nerve.py:119-188) --------------------
+ * Writes "[{...},...]": per node, keys sorted (composition, element,
+ * filter_mean, id, rows, size, stats), floats "%.9g" with "-0" -> "0",
+ * non-finite -> BM_ERR_DATA. Host memory only (no device work):
+ *   h_node_rows/h_node_off  rows of node v: [off[v], off[v+1])
+ *   h_elem                  2 per node: element index, or (i, j) for 2-D covers
+ *                           (second value -1 for 1-D)
+ *   h_stats (n_nodes x d)   column means; h_stat_order[i] = column of the i-th
+ *                           key in sorted key order, h_names[h_name_off[i] ..
+ *                           h_name_off[i+1]) its JSON-quoted name
+ *   h_fmean (n_nodes x m)   filter means
+ *   h_comp/h_comp_off       per node, the JSON text of its composition object
+ * Call with out == NULL to get the length in *h_len, then with a buffer of at
+ * least that many bytes. */
+int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows, const int64_t* h_node_off,
+                  const int32_t* h_elem, const double* h_stats, int64_t d,
+                  const int32_t* h_stat_order, const char* h_names, const int64_t* h_name_off,
+                  const double* h_fmean, int32_t m, const char* h_comp,
+                  const int64_t* h_comp_off, char* out, int64_t cap, int64_t* h_len);
+
 /* ---- node payload (nerve.py:60-62, 96) --------------------------------------
  * d_stats[v*d + c] = numpy mean over node v's rows of column c (sequential
  * row sum / size, as numpy's axis-0 mean); d_fmean[v*m + a] = numpy 1-D mean

@@ -64,6 +64,8 @@ _SIGNATURES = {
     "bm_merge_forest": (ctypes.c_int, [_vp, _vp, _c_i64, _vp]),
     "bm_group_nodes": (ctypes.c_int, [_vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bm_nerve_edges": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),
+    "bm_json_nodes": (ctypes.c_int, [_c_i64, _vp, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _vp,
+                                     _c_i32, _vp, _vp, _vp, _c_i64, _vp]),
     "bm_node_stats": (ctypes.c_int, [_vp, _c_i64, _vp, ctypes.c_int, _vp, _vp, _c_i64, _vp, _vp, _vp]),
 }
 

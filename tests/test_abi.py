@@ -88,3 +88,40 @@ def test_no_gpu_means_loud_failure():
     with pytest.raises(InternalError):
         evaluate(pc, FilterSpec(kind="l2-norm"))
     assert not issubclass(InternalError, DataError)
+
+
+def test_native_graph_json_matches_python_writer():
+    """bm_json_nodes (host code, no GPU) writes the node array byte-identically
+    to the Python canonical writer, floats included ("%.9g", -0 -> 0)."""
+    import numpy as np
+
+    from paper_2011_03209_b200.nerve import assemble_graph, graph_to_json, graph_to_obj
+    from paper_2011_03209_b200.nerve import to_canonical_json
+
+    class PC:
+        numerical_columns = ["b", "a", "Z", "x_1", "é"]
+        categorical_columns = []
+
+    class Cov:
+        def __init__(self, two_d):
+            self.two_d = two_d
+
+        def element_key(self, k):
+            return [k // 3, k % 3] if self.two_d else k
+
+    rng = np.random.default_rng(7)
+    specials = [0.0, -0.0, 1e-5, 9.99999999e-5, 1e-4, 123456789.0, 1234567890.0, 1e16,
+                -2.5e-300, 5e-324, 1.7976931348623157e308, 0.1, 1 / 3, -7.0, 100.0]
+    for two_d in (False, True):
+        n_nodes = 40
+        sizes = rng.integers(1, 60, n_nodes)
+        off = np.zeros(n_nodes + 1, dtype=np.int64)
+        np.cumsum(sizes, out=off[1:])
+        rows = np.concatenate([np.sort(rng.choice(10 ** 6, s, replace=False)) for s in sizes])
+        stats = rng.standard_normal((n_nodes, 5)) * 10.0 ** rng.integers(-12, 12, (n_nodes, 5))
+        stats.flat[: len(specials)] = specials
+        fmean = rng.standard_normal((n_nodes, 2)) * 1e3
+        g = assemble_graph(PC(), None, Cov(two_d), {"k": [1, 2.5], "s": "x"}, rows, off,
+                           np.arange(n_nodes), stats, fmean,
+                           np.array([[0, 1, 3], [2, 5, 1]], dtype=np.int64))
+        assert graph_to_json(g) == to_canonical_json(graph_to_obj(g))

@@ -250,28 +250,72 @@ __global__ void node_stats_kernel(const double* __restrict__ X, int64_t d,
   stats[v * d + c] = __ddiv_rn(s, (double)(b - a));
 }
 
-__device__ double pairwise_gather(const double* __restrict__ f, int m, int ax,
-                                  const int64_t* __restrict__ rows, int64_t n) {
+// numpy pairwise_sum (loops_utils.h.src) over f[rows[i] * m + ax], i < n:
+// a leaf of <= 128 terms uses 8 strided accumulators (plain loop below 8);
+// larger ranges split at n2 = n/2 - (n/2)%8. The recursion is emulated with an
+// explicit stack (device recursion overflows the per-thread stack for nodes
+// of ~100k rows).
+__device__ double pairwise_leaf(const double* __restrict__ f, int m, int ax,
+                                const int64_t* __restrict__ rows, int64_t n) {
   if (n < 8) {
     double r = -0.0;
     for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, f[rows[i] * m + ax]);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = f[rows[j] * m + ax];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f[rows[i + j] * m + ax]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, f[rows[i] * m + ax]);
-    return res;
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = f[rows[j] * m + ax];
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f[rows[i + j] * m + ax]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, f[rows[i] * m + ax]);
+  return res;
+}
+
+__device__ double pairwise_gather(const double* __restrict__ f, int m, int ax,
+                                  const int64_t* __restrict__ rows, int64_t n) {
+  if (n <= 128) return pairwise_leaf(f, m, ax, rows, n);
+  constexpr int kDepth = 48;  // n < 2^40
+  int64_t off_s[kDepth], n_s[kDepth];
+  double left_s[kDepth];
+  bool right_s[kDepth];  // false: left child pending, true: right child pending
+  int sp = 1;
+  off_s[0] = 0;
+  n_s[0] = n;
+  right_s[0] = false;
+  while (true) {
+    const int t = sp - 1;
+    const int64_t o = off_s[t], nn = n_s[t];
+    if (nn > 128) {  // fresh internal node: descend into its left half
+      int64_t n2 = nn / 2;
+      n2 -= n2 % 8;
+      off_s[sp] = o;
+      n_s[sp] = n2;
+      right_s[sp] = false;
+      ++sp;
+      continue;
+    }
+    double val = pairwise_leaf(f, m, ax, rows + o, nn);
+    --sp;
+    while (sp > 0) {  // hand the value to the parents
+      const int p = sp - 1;
+      if (!right_s[p]) {  // left half done: start the right half
+        left_s[p] = val;
+        right_s[p] = true;
+        int64_t n2 = n_s[p] / 2;
+        n2 -= n2 % 8;
+        off_s[sp] = off_s[p] + n2;
+        n_s[sp] = n_s[p] - n2;
+        right_s[sp] = false;
+        ++sp;
+        break;
+      }
+      val = __dadd_rn(left_s[p], val);  // left + right, as the recursion returns
+      --sp;
+    }
+    if (sp == 0) return val;
   }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_gather(f, m, ax, rows, n2),
-                   pairwise_gather(f, m, ax, rows + n2, n - n2));
 }
 
 __global__ void node_fmean_kernel(const double* __restrict__ f, int m,

@@ -140,3 +140,30 @@ def test_exact_distance_orders(dev, d):
     P = X[rows]
     ref = np.stack([np.sqrt(((P - P[i]) * (P - P[i])).sum(axis=1)) for i in range(len(rows))])
     assert np.array_equal(pw, ref)
+
+
+@pytest.mark.parametrize("sizes", [[1, 7, 8, 129, 1000], [250_001, 3, 131_072]])
+def test_node_payload_matches_numpy(dev, sizes):
+    """bm_node_stats: per-column means (numpy axis-0 mean: sequential row sum)
+    and filter means (1-D mean: pairwise sum) bit-exact, including nodes of
+    several hundred thousand rows (deep pairwise recursion)."""
+    import torch
+
+    from paper_2011_03209_b200 import engine as eng
+
+    rng = np.random.default_rng(sum(sizes))
+    n, d, m = 600_000, 5, 2
+    X = rng.standard_normal((n, d)) * 1e3
+    F = rng.standard_normal((n, m)) * 1e6
+    rows = [np.sort(rng.choice(n, s, replace=False)) for s in sizes]
+    off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=off[1:])
+    flat = np.concatenate(rows)
+    st, fm = eng.node_payload(torch.from_numpy(X).to(dev), torch.from_numpy(F).to(dev),
+                              torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev),
+                              len(sizes))
+    st, fm = st.cpu().numpy(), fm.cpu().numpy()
+    for v, r in enumerate(rows):
+        assert np.array_equal(st[v], X[r].mean(axis=0)), v
+        for a in range(m):
+            assert fm[v, a] == F[r, a].mean(), (v, a)

@@ -4,8 +4,12 @@ A step = one full Mapper graph build of the workload: lens -> cover binning
 -> per-element DBSCAN -> nodes -> nerve edges.
   value : points/s with X already resident in HBM (device-timed, CUDA events,
           max over ranks)
-  e2e   : points/s through the public path with HOST buffers: pinned fp64 X
-          copied H2D every step, node rows + edges copied D2H every step
+  e2e   : points/s through the reference-facing call with HOST buffers: on
+          one GPU compute_mapper(pc, params) on page-locked fp64 X, returning
+          the MapperRun with the canonical graph JSON (H2D of X, D2H of the
+          node rows/payload/edges, JSON writing all inside the timed region);
+          on N GPUs the sharded build with X copied H2D and node rows + edges
+          copied D2H every step
 Inputs (2 GB at 1M x 256 fp64) exceed the 126 MB L2, so no flush is needed.
 
   python bench.py [--gpus N --steps K --warmup W --config cfg3 --impl ours|reference]
@@ -315,23 +319,44 @@ def main():
     if g is not None:
         sizes = g.sizes
 
-    # ---- end-to-end timed region (host X in, node rows + edges out)
+    # ---- end-to-end timed region: host X in (page-locked), result out.
+    # One GPU: the reference-facing call itself, compute_mapper(pc, params)
+    # (pipeline.py:81-110) -> MapperRun with the canonical graph JSON bytes.
+    # Several GPUs: the sharded build + read-back of node rows and edges.
     h2d = X.nbytes
     d2h = 0
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
-    Xs = torch.empty_like(Xd)  # the step's input buffer (refilled from host every step)
-    barrier()
-    f0.record(stream)
-    for _ in range(args.steps):
-        Xs.copy_(Xh, non_blocking=True)
-        g2, _ = step(Xs)
-        if g2 is not None:
-            nr = g2.node_rows.cpu()
-            no = g2.node_off.cpu()
-            d2h = nr.numel() * 8 + no.numel() * 8 + g2.edges.nbytes
-    f1.record(stream)
-    barrier()
+    if world == 1:
+        from paper_2011_03209_b200 import compute_mapper, from_array
+
+        pc_host = from_array(Xh.numpy())  # page-locked host buffer, no copy
+        run = compute_mapper(pc_host, params, engine=args.engine)
+        barrier()
+        f0.record(stream)
+        for _ in range(args.steps):
+            run = compute_mapper(pc_host, params, engine=args.engine)
+        f1.record(stream)
+        barrier()
+        gr = run.graph
+        n_rows = sum(len(nd.rows) for nd in gr.nodes)
+        d2h = 8 * (n_rows + gr.n_nodes + 1 + gr.n_nodes * (w.d + len(params.filters)) +
+                   3 * len(gr.edges))
+        e2e_api = "compute_mapper -> MapperRun (graph + canonical JSON bytes)"
+    else:
+        Xs = torch.empty_like(Xd)  # the step's input buffer (refilled from host every step)
+        barrier()
+        f0.record(stream)
+        for _ in range(args.steps):
+            Xs.copy_(Xh, non_blocking=True)
+            g2, _ = step(Xs)
+            if g2 is not None:
+                nr = g2.node_rows.cpu()
+                no = g2.node_off.cpu()
+                d2h = nr.numel() * 8 + no.numel() * 8 + g2.edges.nbytes
+        f1.record(stream)
+        barrier()
+        e2e_api = "build_distributed -> node rows + edges on rank 0"
     t_e2e = max_over_ranks(f0.elapsed_time(f1) / 1e3)
 
     if rank != 0:
@@ -356,7 +381,8 @@ def main():
         else "f64",
         "data": "synthetic", "config": config_of(w, world),
         "e2e": {"value": w.n * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps},
+                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps,
+                "api": e2e_api},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
                      "traffic_note": "DRAM bytes per tc_adjacency_kernel launch, ncu --set full "

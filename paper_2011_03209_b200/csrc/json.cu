@@ -9,7 +9,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -56,22 +58,15 @@ struct Out {
 
 using namespace bm;
 
-extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
-                             const int64_t* h_node_off, const int32_t* h_elem,
-                             const double* h_stats, int64_t d, const int32_t* h_stat_order,
-                             const char* h_names, const int64_t* h_name_off,
-                             const double* h_fmean, int32_t m, const char* h_comp,
-                             const int64_t* h_comp_off, char* out, int64_t cap,
-                             int64_t* h_len) {
-  BM_REQUIRE(n_nodes >= 0 && d >= 0 && m >= 0, "bad sizes");
-  BM_REQUIRE(h_len, "null output length");
-  BM_REQUIRE(n_nodes == 0 || (h_node_rows && h_node_off && h_elem && h_comp && h_comp_off),
-             "null node table");
-  BM_REQUIRE(d == 0 || (h_stats && h_stat_order && h_names && h_name_off), "null stats table");
-  BM_REQUIRE(m == 0 || h_fmean, "null filter means");
-  Out o{out, out ? cap : 0};
-  o.put("[", 1);
-  for (int64_t v = 0; v < n_nodes; ++v) {
+namespace {
+
+// nodes [v0, v1) into o; false on a non-finite value
+bool write_nodes(Out& o, int64_t v0, int64_t v1, const int64_t* h_node_rows,
+                 const int64_t* h_node_off, const int32_t* h_elem, const double* h_stats,
+                 int64_t d, const int32_t* h_stat_order, const char* h_names,
+                 const int64_t* h_name_off, const double* h_fmean, int32_t m, const char* h_comp,
+                 const int64_t* h_comp_off) {
+  for (int64_t v = v0; v < v1; ++v) {
     if (v) o.put(",", 1);
     // keys in sorted order: composition, element, filter_mean, id, rows, size, stats
     o.put("{\"composition\":");
@@ -89,10 +84,7 @@ extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
     o.put(",\"filter_mean\":[");
     for (int32_t a = 0; a < m; ++a) {
       if (a) o.put(",", 1);
-      if (!o.put_num(h_fmean[v * m + a])) {
-        set_error("non-finite value in graph JSON");
-        return BM_ERR_DATA;
-      }
+      if (!o.put_num(h_fmean[v * m + a])) return false;
     }
     o.put("],\"id\":");
     o.put_int(v);
@@ -109,13 +101,71 @@ extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
       const int32_t c = h_stat_order[i];  // i-th key in sorted order -> column
       o.put(h_names + h_name_off[i], h_name_off[i + 1] - h_name_off[i]);  // quoted key
       o.put(":", 1);
-      if (!o.put_num(h_stats[v * d + c])) {
-        set_error("non-finite value in graph JSON");
-        return BM_ERR_DATA;
-      }
+      if (!o.put_num(h_stats[v * d + c])) return false;
     }
     o.put("}}", 2);
   }
+  return true;
+}
+
+}  // namespace
+
+extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
+                             const int64_t* h_node_off, const int32_t* h_elem,
+                             const double* h_stats, int64_t d, const int32_t* h_stat_order,
+                             const char* h_names, const int64_t* h_name_off,
+                             const double* h_fmean, int32_t m, const char* h_comp,
+                             const int64_t* h_comp_off, char* out, int64_t cap,
+                             int64_t* h_len) {
+  BM_REQUIRE(n_nodes >= 0 && d >= 0 && m >= 0, "bad sizes");
+  BM_REQUIRE(h_len, "null output length");
+  BM_REQUIRE(n_nodes == 0 || (h_node_rows && h_node_off && h_elem && h_comp && h_comp_off),
+             "null node table");
+  BM_REQUIRE(d == 0 || (h_stats && h_stat_order && h_names && h_name_off), "null stats table");
+  BM_REQUIRE(m == 0 || h_fmean, "null filter means");
+  // node ranges of balanced byte volume are written by host threads into
+  // private buffers, then concatenated in order
+  const int64_t total = n_nodes ? h_node_off[n_nodes] : 0;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, total / 65536));
+  std::vector<int64_t> cut(nt + 1, n_nodes);
+  cut[0] = 0;
+  for (int t = 1, v = 0; t < nt; ++t) {
+    while (v < n_nodes && h_node_off[v] < total * t / nt) ++v;
+    cut[t] = v;
+  }
+  std::vector<std::vector<char>> parts(nt);
+  std::vector<int> ok(nt, 1);
+  auto work = [&](int t) {
+    const int64_t v0 = cut[t], v1 = std::max(cut[t], cut[t + 1]);
+    const int64_t est = (h_node_off[v1] - h_node_off[v0]) * 8 + (v1 - v0) * (d + m + 8) * 18 + 64;
+    parts[t].resize(est);
+    for (;;) {
+      Out o{parts[t].data(), (int64_t)parts[t].size()};
+      ok[t] = write_nodes(o, v0, v1, h_node_rows, h_node_off, h_elem, h_stats, d, h_stat_order,
+                          h_names, h_name_off, h_fmean, m, h_comp, h_comp_off);
+      if (o.len <= (int64_t)parts[t].size()) {
+        parts[t].resize(o.len);
+        return;
+      }
+      parts[t].resize(o.len);  // estimate too small: rewrite at the exact size
+    }
+  };
+  if (nt == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+  }
+  for (int t = 0; t < nt; ++t)
+    if (!ok[t]) {
+      set_error("non-finite value in graph JSON");
+      return BM_ERR_DATA;
+    }
+  Out o{out, out ? cap : 0};
+  o.put("[", 1);
+  for (int t = 0; t < nt; ++t) o.put(parts[t].data(), (int64_t)parts[t].size());
   o.put("]", 1);
   *h_len = o.len;
   if (out && o.len > cap) {

@@ -42,15 +42,17 @@ def stream_ptr(dev) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
-def to_device_f64(arr: np.ndarray, dev, pinned: bool = True):
+def to_device_f64(arr: np.ndarray, dev):
+    """Device copy of a host fp64 array. Page-locked host memory (e.g. the
+    numpy view of a torch pin_memory() tensor) is copied asynchronously at
+    full PCIe speed; pageable memory goes through the driver's staged copy
+    (pinning it first would cost a fresh page-locked allocation per call)."""
     a = np.ascontiguousarray(arr, dtype=np.float64)
     with warnings.catch_warnings():
         # read-only PointCloud arrays: torch only reads them (H2D source)
         warnings.simplefilter("ignore", UserWarning)
         t = torch.from_numpy(a)
-    if pinned and a.nbytes >= (1 << 20):
-        t = t.pin_memory()
-    return t.to(dev, non_blocking=pinned)
+    return t.to(dev, non_blocking=bool(a.nbytes and t.is_pinned()))
 
 
 def to_device_i64(arr: np.ndarray, dev):

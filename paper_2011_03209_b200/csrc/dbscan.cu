@@ -43,7 +43,6 @@ int tc_collect(TcPrep* tp, int64_t* rechecked, bool* overflow, cudaStream_t stre
 
 namespace {
 
-__constant__ PwProgram c_prog;
 
 // ---------------------------------------------------------------------------
 // gather: Xg[p] = X[rows[ent[p]]] (zero for pads). One warp per padded row.
@@ -733,7 +732,8 @@ template <int DEPTH>
 __global__ void __launch_bounds__(256, 1)
 adjacency_exact_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, double eps,
                        const TileRef* __restrict__ tiles, uint32_t* __restrict__ adj,
-                       int32_t* __restrict__ nonempty, int64_t tile0) {
+                       int32_t* __restrict__ nonempty, int64_t tile0,
+                       const __grid_constant__ PwProgram c_prog) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + kKC * kLd;
@@ -1140,7 +1140,7 @@ inline unsigned grid_for(int64_t n, int threads, int per_sm = 8) {
 template <int DEPTH>
 int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
                        int64_t n_tiles, double eps, uint32_t* adj, int32_t* nonempty,
-                       cudaStream_t stream) {
+                       const PwProgram& prog, cudaStream_t stream) {
   static bool attr_done = false;  // per process; attribute is per function
   if (!attr_done) {
     BM_CHECK_CUDA(cudaFuncSetAttribute(adjacency_exact_kernel<DEPTH>,
@@ -1152,7 +1152,7 @@ int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const 
   for (int64_t t0 = 0; t0 < n_tiles; t0 += kMaxGrid) {
     int64_t nb = std::min<int64_t>(kMaxGrid, n_tiles - t0);
     adjacency_exact_kernel<DEPTH><<<(unsigned)nb, 256, kExactSmem, stream>>>(
-        Xg, d, et, eps, tiles, adj, nonempty, t0);
+        Xg, d, et, eps, tiles, adj, nonempty, t0, prog);
     BM_CHECK_LAUNCH();
   }
   return BM_OK;
@@ -1164,21 +1164,20 @@ int exact_build_adjacency(const double* Xg, int64_t d, const ElemTables& et, con
   if (n_tiles == 0) return BM_OK;
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
-  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
-                                        stream));
   switch (prog.depth) {
-    case 1: return launch_exact_depth<1>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
-    case 2: return launch_exact_depth<2>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
-    case 3: return launch_exact_depth<3>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
-    case 4: return launch_exact_depth<4>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
-    default: return launch_exact_depth<kMaxStack>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, stream);
+    case 1: return launch_exact_depth<1>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, prog, stream);
+    case 2: return launch_exact_depth<2>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, prog, stream);
+    case 3: return launch_exact_depth<3>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, prog, stream);
+    case 4: return launch_exact_depth<4>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, prog, stream);
+    default: return launch_exact_depth<kMaxStack>(Xg, d, et, tiles, n_tiles, eps, adj, nonempty, prog, stream);
   }
 }
 
 // full distance matrix of a row subset in one exact order (API helper)
 __global__ void pairwise_matrix_kernel(const double* __restrict__ X, int64_t d,
                                        const int64_t* __restrict__ rows, int64_t n, int order,
-                                       double* __restrict__ out) {
+                                       double* __restrict__ out,
+                                       const __grid_constant__ PwProgram c_prog) {
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / n, j = idx - i * n;
@@ -1985,10 +1984,8 @@ extern "C" int bm_pairwise_distances(const double* d_X, int64_t n, int64_t d,
   BM_REQUIRE(d_X && d_rows && d_out, "null pointer");
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
-  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog, &prog, sizeof(prog), 0, cudaMemcpyHostToDevice,
-                                        stream));
   pairwise_matrix_kernel<<<grid_for(n_rows * n_rows, 128, 32), 128, 0, stream>>>(
-      d_X, d, d_rows, n_rows, order, d_out);
+      d_X, d, d_rows, n_rows, order, d_out, prog);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }

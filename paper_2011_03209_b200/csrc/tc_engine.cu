@@ -73,7 +73,6 @@ constexpr int kLimb = 7;        // bits of the M and L limbs
 constexpr int kQBits = 2 * kLimb + 7;   // |q| <= 2^21 - 1: H = q >> 14 is a signed byte
 constexpr int kYShift = 3 * kLimb + 1;  // y is in units of 2^22 of D2
 
-__constant__ PwProgram c_prog_tc;
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -889,7 +888,7 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
                    const int4* __restrict__ queue, const unsigned long long* __restrict__ nq_ptr,
                    unsigned long long qcap, double eps,
                    uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
-                   int32_t* __restrict__ cnt,
+                   int32_t* __restrict__ cnt, const __grid_constant__ PwProgram c_prog_tc,
                    unsigned long long* __restrict__ n_inside) {
   __shared__ double sq_all[kRcWarps][32][33];
   const int64_t nq = (int64_t)(*nq_ptr < qcap ? *nq_ptr : qcap);
@@ -1069,6 +1068,8 @@ bool tc_supported(int64_t d) { return d >= 32 && d <= 256; }
 struct TcPrep {
   int64_t d = 0, P = 0, n_el = 0, n_tiles = 0, kpad = 0;
   int nkc = 0, depth = 1;  // depth: pairwise-sum stack depth of d (PwProgram)
+  PwProgram prog{};       // numpy pairwise-sum program of d (a kernel argument: no
+                          // shared constant memory, so concurrent calls are safe)
   double eps = 0.0;
   std::vector<int32_t> nrows;
   Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw, s_flag;
@@ -1093,8 +1094,6 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   BM_REQUIRE(nkc >= 1 && nkc <= 2, "tensor-core engine supports d <= 256");
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
-  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog_tc, &prog, sizeof(prog), 0,
-                                        cudaMemcpyHostToDevice, stream));
   TcPrep* tp = new TcPrep();
   struct Guard {
     TcPrep*& p;
@@ -1107,6 +1106,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   tp->kpad = kpad;
   tp->nkc = nkc;
   tp->depth = prog.depth;
+  tp->prog = prog;
   tp->eps = eps;
   tp->nrows = h_nrows;
   const int64_t n_tiles = P / kTile;
@@ -1328,15 +1328,18 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     switch (tp->depth) {
       case 1:
         recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, cnt_run, d_cnt + 1);
+                                                            adj, nonempty, cnt_run, tp->prog,
+                                                            d_cnt + 1);
         break;
       case 2:
         recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, cnt_run, d_cnt + 1);
+                                                            adj, nonempty, cnt_run, tp->prog,
+                                                            d_cnt + 1);
         break;
       default:
         recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, cnt_run, d_cnt + 1);
+                                                            adj, nonempty, cnt_run, tp->prog,
+                                                            d_cnt + 1);
         break;
     }
     BM_CHECK_LAUNCH();

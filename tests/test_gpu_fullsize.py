@@ -156,3 +156,49 @@ def test_cfg5_row_block_element_sampled():
         got = [c.tolist() for c in _element_clusters(g, int(k))]
         assert sum(len(c) for c in got) <= rows.size
         _check_sampled(X, w, g, int(k), rows, got, rng, n_sample=8)
+
+
+def test_cfg4_pca_grid_library_pieces():
+    """cfg4 (500k x 128, 2-D PCA lens as FilterValues, 15 x 15 cover, eps 14.7)
+    through the library pieces (test_nerve.py:23-30's composition): memberships
+    equal the oracle's 2-D intersection, elements <= 3000 rows equal the
+    oracle's DBSCAN, larger ones obey the sampled DBSCAN rules."""
+    import time
+
+    from paper_2011_03209_b200 import (DbscanParams, DistanceStrategy, FilterSpec, FilterValues,
+                                       build_cover, cluster_all, from_array, membership)
+    from paper_2011_03209_b200 import workloads
+
+    w = workloads.CONFIGS["cfg4"]
+    X = workloads.points(w)
+    Xc = X - X.mean(axis=0)
+    _, _, vt = np.linalg.svd(Xc[:20000], full_matrices=False)
+    F = np.ascontiguousarray(Xc @ vt[:2].T)
+    pc = from_array(X)
+    fv = FilterValues(values=F.copy(), specs=[FilterSpec(kind="l2-norm")] * 2)
+    t0 = time.time()
+    cover = build_cover(fv, list(w.intervals), list(w.overlaps))
+    members = membership(fv, cover)
+    cl = cluster_all(pc, members, DbscanParams(w.eps, w.min_pts),
+                     DistanceStrategy(threshold=10 ** 9))
+    print(f"cfg4 library pieces: {time.time() - t0:.3f} s, "
+          f"{sum(len(c.clusters) for c in cl)} clusters")
+    axes = [O.cover_axis(F[:, a], w.intervals[a], w.overlaps[a]) for a in range(2)]
+    want = O.membership(F, axes)
+    assert [m.tolist() for m in members] == [m.tolist() for m in want]
+    g = dict(orders=np.zeros(len(members), dtype=np.uint8))  # threshold 1e9: cdist order
+    rng = np.random.default_rng(4)
+    checked_small = checked_large = 0
+    for k, rows in enumerate(members):
+        rows = np.asarray(rows, dtype=np.int64)
+        if rows.size == 0:
+            continue
+        got = [list(c) for c in cl[k].clusters]
+        if rows.size <= 3000:
+            clusters, noise = O.dbscan_element(X, rows, w.eps, w.min_pts, O.ORDER_SEQUENTIAL)
+            assert got == clusters and list(cl[k].noise) == noise, k
+            checked_small += 1
+        else:
+            _check_sampled(X, w, g, k, rows, got, rng, n_sample=8)
+            checked_large += 1
+    assert checked_small >= 5 and checked_large >= 5

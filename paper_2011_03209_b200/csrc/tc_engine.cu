@@ -13,7 +13,7 @@
 // shift class in three TMEM accumulators (N = 128 columns each):
 //   A0 = H.H   A1 = H.M + M.H   A2 = H.L + M.M + L.H
 // The omitted A3 = M.L + L.M and L.L terms are non-negative and bounded
-// (prm.a3max, prm.ll2), so D2c = N_i + N_j - 2 (A0<<28 + A1<<21 + A2<<14)
+// (Cauchy-Schwarz on per-tile limb norms), so D2c = N_i + N_j - 2 (A0<<28 + A1<<21 + A2<<14)
 // brackets D2_q = |q_i - q_j|^2 from both sides with known slack.
 // Per point the quantisation error e_i = |x_i - c - s q_i| is measured in
 // fp64 (tile maxima, tile_u); by the triangle inequality
@@ -207,8 +207,7 @@ struct TcParams {
   const int32_t* tbase;   // per element: first global 128-row tile index
   const double* a_in;     // per element: eps / (1 + gamma) / s_k
   const double* a_out;    // per element: eps / (1 - gamma) / s_k
-  double ll2;             // 2 * 255^2 * Kpad (bound of the omitted L.L term in D2)
-  double a3max;           // 2^9 * 2 * 255^2 * Kpad (bound of the A3 term in D2)
+  const uint32_t* limb_sq;  // per 128-row tile: max over rows of |M|^2, |L|^2 (limb planes)
   int nkc;                // Kpad / 128
   uint32_t* adj;
   int32_t* nonempty;      // per window slot: 1 if the tile holds any bit (zeroed by the host)
@@ -223,6 +222,21 @@ struct TcParams {
 
 constexpr double kBig = 4.0e18;
 
+// Bounds of the omitted non-negative terms from the tiles' limb norms
+// (Cauchy-Schwarz): L.L <= |L_i||L_j|, A3 = M.L + L.M <= |M_i||L_j| + |L_i||M_j|,
+// rounded up (per-tile maxima of the row norms; far below the worst case
+// 127^2 Kpad, which narrows the recheck band ~3x).
+__device__ __forceinline__ double limb_norm(const TcParams& P, int64_t t, int which) {
+  return __dsqrt_ru((double)P.limb_sq[2 * t + which]);
+}
+__device__ __forceinline__ double ll_bound(const TcParams& P, int64_t tI, int64_t tJ) {
+  return __dmul_ru(limb_norm(P, tI, 1), limb_norm(P, tJ, 1)) * (1.0 + 1e-12);
+}
+__device__ __forceinline__ double a3_bound(const TcParams& P, int64_t tI, int64_t tJ) {
+  return __dadd_ru(__dmul_ru(limb_norm(P, tI, 0), limb_norm(P, tJ, 1)),
+                   __dmul_ru(limb_norm(P, tI, 1), limb_norm(P, tJ, 0))) * (1.0 + 1e-12);
+}
+
 // fp64 thresholds on D2c for one (row tile, column tile) pair; the +-64
 // margins cover the fp64 rounding of S = N_i + N_j and of the fast D2.
 __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI, int64_t tJ,
@@ -236,14 +250,15 @@ __device__ __forceinline__ void thresholds(const TcParams& P, int k, int64_t tI,
   const double ri = P.a_in[k] - du;
   t_in = ri > 0.0 ? ri * ri * (1.0 - 1e-12) - 64.0 : -kBig;
   const double ro = P.a_out[k] + du;
-  t_out = ro * ro * (1.0 + 1e-12) + P.ll2 + 64.0;
+  t_out = ro * ro * (1.0 + 1e-12) + 2.0 * ll_bound(P, tI, tJ) + 64.0;
 }
 
 // Per bitmap tile pair: exact thresholds t_in/t_out on D2c and the integer
 // offsets of the fast path (see the epilogue): with U = 2^kYShift and
 // niU = floor(N_i/U),
 //   r_in  = niU + ceil(-t_in/U) + 3   >= (N_i - t_in)/U + 2
-//   r_out = niU + floor(-(t_out + a3max)/U) - 2 <= (N_i - t_out - a3max)/U - 1
+//   r_out = niU + floor(-(t_out + a3)/U) - 2 <= (N_i - t_out - a3)/U - 1
+// with a3 = 2^(kLimb+1) a3_bound (the A3 term's weight in D2).
 __global__ void tile_thr_kernel(TcParams P, int64_t n_tiles, TileThr* __restrict__ out) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_tiles) return;
@@ -259,7 +274,8 @@ __global__ void tile_thr_kernel(TcParams P, int64_t n_tiles, TileThr* __restrict
                          : kNever;
   // clamping k_in down is conservative (fewer certain-inside pairs); k_out
   // must never be raised, so out-of-range values disable the certain-outside test
-  const double ko = floor(-(t_out + P.a3max) * sc) - 2.0;
+  const double a3 = (double)(2 << kLimb) * a3_bound(P, P.tbase[k] + I, P.tbase[k] + J);
+  const double ko = floor(-(t_out + a3) * sc) - 2.0;
   th.k_out = (t_out < 1e18 && ko >= -1073741824.0) ? (int32_t)ko : kNever;
   out[g] = th;
 }
@@ -764,7 +780,8 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
                                 int64_t* __restrict__ nq, int32_t* __restrict__ cq,
                                 unsigned long long* __restrict__ tile_e,
                                 const double* __restrict__ cen,
-                                unsigned long long* __restrict__ rad_bits) {
+                                unsigned long long* __restrict__ rad_bits,
+                                uint32_t* __restrict__ limb_sq) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
@@ -782,6 +799,7 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
     const double* ck = center + (int64_t)k * d;
     const double* ct = cen ? cen + (p / kTile) * d : nullptr;
     long long nsum = 0;
+    uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
     double esum = 0.0, ysum = 0.0, rsum = 0.0;
     for (int64_t c4 = 4 * lane; c4 < kpad; c4 += 128) {
       uint32_t hw = 0, mw = 0, lw = 0;
@@ -804,6 +822,9 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
           }
         }
         nsum += (long long)q * q;
+        const uint32_t mq = (q >> kLimb) & ((1 << kLimb) - 1), lq = q & ((1 << kLimb) - 1);
+        msq += mq * mq;
+        lsq += lq * lq;
         hw |= (uint32_t)(uint8_t)(int8_t)(q >> (2 * kLimb)) << (8 * j);
         mw |= (uint32_t)((q >> kLimb) & ((1 << kLimb) - 1)) << (8 * j);
         lw |= (uint32_t)(q & ((1 << kLimb) - 1)) << (8 * j);
@@ -817,10 +838,14 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
       esum += __shfl_xor_sync(0xffffffffu, esum, o);
       ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
       rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+      msq += __shfl_xor_sync(0xffffffffu, msq, o);
+      lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
     }
     if (lane == 0) {
       nq[p] = nsum;
       cq[p] = (int32_t)(nsum >> kYShift);
+      atomicMax(limb_sq + 2 * (p / kTile), msq);  // pads are all-zero rows
+      atomicMax(limb_sq + 2 * (p / kTile) + 1, lsq);
       if (valid) {
         // rigorous upper bound of |x - c - s q|: the fp64 evaluation of each
         // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
@@ -1072,7 +1097,7 @@ struct TcPrep {
                           // shared constant memory, so concurrent calls are safe)
   double eps = 0.0;
   std::vector<int32_t> nrows;
-  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw, s_flag;
+  Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw, s_flag, s_lim;
   // deferred recheck-queue check: [0] largest overflowing request, [1] pairs
   // rechecked (device); the caller reads them at its next synchronisation
   unsigned long long* d_flag = nullptr;
@@ -1143,10 +1168,12 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
                                                         scale);
   BM_CHECK_LAUNCH();
   if (rad) BM_CHECK_CUDA(cudaMemsetAsync(rad, 0, n_tiles * 8, stream));
+  BM_TRY(scratch_alloc(tp->s_lim, (size_t)n_tiles * 8, stream));
+  BM_CHECK_CUDA(cudaMemsetAsync(tp->s_lim.ptr, 0, n_tiles * 8, stream));
   quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
       Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
       reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
-      cen, reinterpret_cast<unsigned long long*>(rad));
+      cen, reinterpret_cast<unsigned long long*>(rad), tp->s_lim.as<uint32_t>());
   BM_CHECK_LAUNCH();
   BM_TRY(make_qmap(&tp->qmap, tp->s_pl.ptr, P, kpad));
 
@@ -1256,9 +1283,7 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     prm.tbase = tp->d_tbase;
     prm.a_in = tp->a_in;
     prm.a_out = tp->a_out;
-    const double lmax = (double)((1 << kLimb) - 1);
-    prm.ll2 = 2.0 * lmax * lmax * (double)tp->kpad;                           // 2 L.L
-    prm.a3max = (double)(2 << kLimb) * 2.0 * lmax * lmax * (double)tp->kpad;  // 2^(b+1) A3
+    prm.limb_sq = tp->s_lim.as<uint32_t>();
     prm.nkc = nkc;
     prm.adj = adj;
     prm.nonempty = nonempty;

@@ -80,6 +80,28 @@ int bm_lens_f64(int kind, const double* d_X, int64_t n, int64_t d, int64_t col,
 int bm_normalize_f64(int scheme, const double* d_X, int64_t n, int64_t d,
                      double* d_out, void* stream);
 
+/* ---- O(N x M) lenses (filters.py:103-150): eccentricity and density ------
+ * For every query row (d_qrows, nq; NULL = rows 0..nq-1) against the target
+ * rows (d_trows, m; NULL = rows 0..m-1; the reference uses all points, or its
+ * seed-1729 subsample of 50k rows when N is larger), with d = scipy cdist:
+ *   BM_PLENS_ECC_MEAN  mean_j d             (eccentricity p = 1; bit-exact)
+ *   BM_PLENS_ECC_RMS   sqrt(mean_j d^2)     (p = 2; bit-exact)
+ *   BM_PLENS_ECC_POW   (mean_j d^p)^(1/p)   (param = p; ulp-level: CUDA pow)
+ *   BM_PLENS_ECC_MAX   max_j d              (p = inf; bit-exact)
+ *   BM_PLENS_DENSITY   sum_j exp(-(d^2)/param), param = 2 sigma^2 (ulp-level: exp)
+ *   BM_PLENS_NN_MIN    min over targets with a different row id (bit-exact;
+ *                      the default bandwidth's nearest-neighbour step)
+ * Sums and means follow numpy's pairwise row reduction over the targets. */
+#define BM_PLENS_ECC_MEAN 0
+#define BM_PLENS_ECC_RMS 1
+#define BM_PLENS_ECC_POW 2
+#define BM_PLENS_ECC_MAX 3
+#define BM_PLENS_DENSITY 4
+#define BM_PLENS_NN_MIN 5
+int bm_pairwise_lens(int kind, double param, const double* d_X, int64_t n, int64_t d,
+                     const int64_t* d_qrows, int64_t nq, const int64_t* d_trows, int64_t m,
+                     double* d_out, void* stream);
+
 /* ---- K2: cover binning (cover.py:122-140, membership) -----------------------
  * f: n x m row-major fp64 filter values (m = 1 or 2).
  * h_lo/h_hi: concatenated per-axis closed-interval endpoints

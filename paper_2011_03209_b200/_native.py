@@ -31,6 +31,13 @@ LENS_COLUMN = 0
 LENS_L2 = 1
 LENS_LINF = 2
 
+PLENS_ECC_MEAN = 0
+PLENS_ECC_RMS = 1
+PLENS_ECC_POW = 2
+PLENS_ECC_MAX = 3
+PLENS_DENSITY = 4
+PLENS_NN_MIN = 5
+
 ENGINE_AUTO = 0
 ENGINE_EXACT = 1
 ENGINE_TC = 2
@@ -47,6 +54,8 @@ _SIGNATURES = {
     "bm_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "bm_device_free_bytes": (ctypes.c_int, [_vp]),
     "bm_lens_f64": (ctypes.c_int, [ctypes.c_int, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp]),
+    "bm_pairwise_lens": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_i64, _c_i64, _vp,
+                                        _c_i64, _vp, _c_i64, _vp, _vp]),
     "bm_normalize_f64": (ctypes.c_int, [ctypes.c_int, _vp, _c_i64, _c_i64, _vp, _vp]),
     "bm_membership_count": (ctypes.c_int, [_vp, _c_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
     "bm_membership_fill": (ctypes.c_int, [_vp, _c_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]),

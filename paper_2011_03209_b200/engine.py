@@ -29,6 +29,33 @@ def lens(X: torch.Tensor, kind: int, col: int = 0) -> torch.Tensor:
     return out
 
 
+def pairwise_lens(X: torch.Tensor, kind: int, param: float, qrows=None, trows=None) -> torch.Tensor:
+    """O(N x M) lens values (filters.py:103-150) of the query rows (default:
+    all) against the target rows (default: all); see bm_pairwise_lens."""
+    n, d = X.shape
+    nq = n if qrows is None else int(qrows.numel())
+    m = n if trows is None else int(trows.numel())
+    out = torch.empty(max(nq, 1), dtype=torch.float64, device=X.device)
+    rc = _native.load().bm_pairwise_lens(int(kind), ctypes.c_double(float(param)), P(X), n, d,
+                                         P(qrows), nq, P(trows), m, P(out),
+                                         stream_ptr(X.device))
+    _native.check(rc, "pairwise lens")
+    return out[:nq]
+
+
+def mean_1d(v: torch.Tensor) -> torch.Tensor:
+    """numpy's 1-D mean (pairwise sum / n) of a device vector, as a 1-element
+    device tensor (bm_node_stats' filter-mean path with one node)."""
+    n = int(v.numel())
+    rows = torch.arange(n, dtype=torch.int64, device=v.device)
+    off = torch.tensor([0, n], dtype=torch.int64, device=v.device)
+    fm = torch.empty(1, dtype=torch.float64, device=v.device)
+    rc = _native.load().bm_node_stats(0, 1, P(v.contiguous()), 1, P(rows), P(off), 1, 0, P(fm),
+                                      stream_ptr(v.device))
+    _native.check(rc, "mean")
+    return fm
+
+
 def normalize(X: torch.Tensor, scheme: str) -> torch.Tensor:
     """dataset.py:165-186 on the device; 'none' returns X itself."""
     if scheme == "none":

@@ -250,13 +250,21 @@ def main():
 
     import torch
 
+    # B200MAP_DIST_BACKEND=gloo runs the N-rank code path on fewer GPUs (ranks
+    # share devices; functional check only — every timing uses NCCL, 1 GPU/rank)
+    backend = os.environ.get("B200MAP_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     os.environ.setdefault("B200MAP_DEVICE", str(local))
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2011_03209_b200 import _native, engine as eng
     from paper_2011_03209_b200.device import require_gpu
     from paper_2011_03209_b200.distributed import build_distributed
@@ -284,6 +292,13 @@ def main():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
+
+    def sum_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
 
     def max_over_ranks(x):
         if dist is None:
@@ -358,6 +373,10 @@ def main():
         barrier()
         e2e_api = "build_distributed -> node rows + edges on rank 0"
     t_e2e = max_over_ranks(f0.elapsed_time(f1) / 1e3)
+    # collectives every rank joins before rank 0 alone reports
+    pairs_all = sum_over_ranks(pairs_eval)
+    tiles_tot = sum_over_ranks(tiles_tot)
+    tiles_skip = sum_over_ranks(tiles_skip)
 
     if rank != 0:
         if dist is not None:
@@ -369,8 +388,9 @@ def main():
     # the distance stage computes only the tile pairs the centroid/radius bound
     # cannot exclude: its algorithmic work is one d-dim dot product (2d flop)
     # per distinct row pair inside those tiles (pairs_eval, from the engine)
-    F_exec = 2.0 * w.d * max_over_ranks(pairs_eval) / args.steps
-    achieved = F_exec / adj_s / 1e12 if adj_s > 0 else 0.0
+    F_exec = 2.0 * w.d * pairs_all / args.steps  # all ranks' executed pair work per step
+    # per GPU: the ranks' work over the slowest rank's distance-stage time
+    achieved = F_exec / world / adj_s / 1e12 if adj_s > 0 else 0.0
     peak = p.get("bf16_tflops_sustained", 1384.6)
     value = w.n * args.steps / t_dev
     line = {

@@ -32,7 +32,7 @@ bool tc_supported(int64_t d);
 struct TcPrep;
 int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
                const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
-               double* cen, double* rad);
+               double* cen, double* rad, const double* tminmax);
 void tc_release(TcPrep* tp);
 int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
@@ -62,6 +62,45 @@ __global__ void gather_kernel(const double* __restrict__ X, int64_t d,
     } else {
       for (int64_t c = lane; c < d; c += 32) dst[c] = 0.0;
     }
+  }
+}
+
+// Gather fused with the per-tile column statistics the tensor-core engine
+// needs (min, max, mean = the tile centre of the pruning bound): one CTA per
+// 128-row tile, one thread per column, rows in order.
+__global__ void __launch_bounds__(256)
+gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                    ElemTables et, double* __restrict__ Xg, double* __restrict__ tmin,
+                    double* __restrict__ tmax, double* __restrict__ cen) {
+  const int64_t tile = blockIdx.x;
+  const int64_t p0 = tile * kTile;
+  __shared__ int64_t src[kTile];
+  __shared__ int nvalid;
+  if (threadIdx.x == 0) nvalid = 0;
+  __syncthreads();
+  if (threadIdx.x < kTile) {
+    const int e = et.ent[p0 + threadIdx.x];
+    src[threadIdx.x] = e >= 0 ? rows[e] : -1;
+    if (e >= 0) atomicAdd(&nvalid, 1);
+  }
+  __syncthreads();
+  const int valid = nvalid;  // valid rows are the tile's first rows (pads at the end)
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn, sm = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < kTile; ++r) {
+      double v = 0.0;
+      if (r < valid) {
+        v = X[src[r] * d + c];
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+        sm += v;
+      }
+      Xg[(p0 + r) * d + c] = v;
+    }
+    tmin[tile * d + c] = mn;
+    tmax[tile * d + c] = mx;
+    cen[tile * d + c] = sm / (double)valid;
   }
 }
 
@@ -1366,8 +1405,22 @@ struct BatchCtx {
     trace_mark("setup:grouped", stream);
     // ---- gather rows (fp64, padded order)
     BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
-    gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
-                                                          xg.as<double>());
+    // tile centres / radii for the pruning bound; with the tensor-core engine
+    // the centres (and the column ranges of the quantisation) come out of the
+    // gather itself, the radii out of the quantisation pass
+    if (prune) BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
+    double* cen = prune ? s_geo.as<double>() : nullptr;
+    double* rad = prune ? cen + n_rt * d : nullptr;
+    Scratch s_mm;
+    if (use_tc && prune) {
+      BM_TRY(scratch_alloc(s_mm, (size_t)n_rt * d * 16, stream));
+      gather_tiles_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
+          d_X, d, rows_b, et, xg.as<double>(), s_mm.as<double>(), s_mm.as<double>() + n_rt * d,
+          cen);
+    } else {
+      gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
+                                                            xg.as<double>());
+    }
     BM_CHECK_LAUNCH();
 
     // ---- per-row work arrays (counts accumulate over the adjacency windows)
@@ -1383,14 +1436,10 @@ struct BatchCtx {
     core = (uint8_t*)(hscan + P + 1);
     BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cmin, 0x7f, P * 4, stream));
-    // tile centres / radii for the pruning bound: fused into the tensor-core
-    // engine's quantisation pass, else a separate pass (build_tiles)
-    if (prune) BM_TRY(scratch_alloc(s_geo, (size_t)n_rt * (d + 1) * 8, stream));
-    double* cen = prune ? s_geo.as<double>() : nullptr;
-    double* rad = prune ? cen + n_rt * d : nullptr;
     trace_mark("setup:gathered", stream);
     if (use_tc) {
-      BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad));
+      const double* tmm = s_mm.ptr ? s_mm.as<double>() : nullptr;
+      BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad, tmm));
       tc_set_queue_scale(tc, qscale);
     }
 

@@ -739,35 +739,50 @@ __global__ void tile_minmax_kernel(const double* __restrict__ Xg, int64_t d, Ele
 }
 
 // per element: centre c = (min+max)/2 per column, half-range R, scale s
-__global__ void elem_scale_kernel(int64_t d, ElemTables et, const int32_t* __restrict__ tbase,
-                                  const double* __restrict__ tmin,
-                                  const double* __restrict__ tmax, double* __restrict__ center,
-                                  double* __restrict__ scale) {
+// per element: centre c = (min+max)/2 per column (CTA per element x 32
+// columns, 8 tile strides reduced in smem) and the half-range R (max over
+// columns, atomicMax on the non-negative double's bits)
+__global__ void __launch_bounds__(256)
+elem_center_kernel(int64_t d, ElemTables et, const int32_t* __restrict__ tbase,
+                   const double* __restrict__ tmin, const double* __restrict__ tmax,
+                   double* __restrict__ center, unsigned long long* __restrict__ rbits) {
   const int k = blockIdx.x;
+  const int lane = threadIdx.x & 31, tg = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.y * 32 + lane;
   const int64_t t0 = tbase[k], t1 = tbase[k] + et.ntiles[k];
-  __shared__ double red[256];
-  double R = 0.0;
-  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
-    for (int64_t t = t0; t < t1; ++t) {
+  __shared__ double smn[8][32], smx[8][32];
+  double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+  if (c < d)
+    for (int64_t t = t0 + tg; t < t1; t += 8) {
       mn = fmin(mn, tmin[t * d + c]);
       mx = fmax(mx, tmax[t * d + c]);
     }
-    double cc = t1 > t0 ? 0.5 * mn + 0.5 * mx : 0.0;
-    if (!(cc == cc) || t1 == t0) cc = 0.0;
-    center[(int64_t)k * d + c] = cc;
-    if (t1 > t0) R = fmax(R, fmax(mx - cc, cc - mn));
-  }
-  red[threadIdx.x] = R;
+  smn[tg][lane] = mn;
+  smx[tg][lane] = mx;
   __syncthreads();
-  for (int o = blockDim.x / 2; o; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
-    __syncthreads();
+  if (tg == 0) {
+    for (int i = 1; i < 8; ++i) {
+      mn = fmin(mn, smn[i][lane]);
+      mx = fmax(mx, smx[i][lane]);
+    }
+    double R = 0.0;
+    if (c < d) {
+      double cc = t1 > t0 ? 0.5 * mn + 0.5 * mx : 0.0;
+      if (!(cc == cc) || t1 == t0) cc = 0.0;
+      center[(int64_t)k * d + c] = cc;
+      if (t1 > t0) R = fmax(fmax(mx - cc, cc - mn), 0.0);
+    }
+    for (int o = 16; o; o >>= 1) R = fmax(R, __shfl_xor_sync(0xffffffffu, R, o));
+    if (lane == 0 && R > 0.0) atomicMax(rbits + k, (unsigned long long)__double_as_longlong(R));
   }
-  if (threadIdx.x == 0) {
-    double Rk = red[0] * (1.0 + 1e-12);
-    scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
-  }
+}
+
+__global__ void elem_scale_kernel(int64_t n_el, const unsigned long long* __restrict__ rbits,
+                                  double* __restrict__ scale) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_el) return;
+  const double Rk = __longlong_as_double((long long)rbits[k]) * (1.0 + 1e-12);
+  scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
 }
 
 // one warp per padded row: limbs into the three planes (4 columns per lane,
@@ -1110,9 +1125,11 @@ struct TcPrep {
   CUtensorMap qmap;
 };
 
+// tminmax (optional): per-tile column min [n_tiles][d] then max, and cen the
+// tile centres, already computed (by the fused gather)
 int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
                const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
-               double* cen, double* rad) {
+               double* cen, double* rad, const double* tminmax) {
   *out = nullptr;
   const int64_t kpad = ceil_div(d, kKC) * kKC;
   const int nkc = (int)(kpad / kKC);
@@ -1149,9 +1166,13 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
                                 cudaMemcpyHostToDevice, stream));
   BM_CHECK_CUDA(cudaMemcpyAsync(tp->d_tbase, tbase.data(), (n_el + 1) * 4, cudaMemcpyHostToDevice,
                                 stream));
-  BM_TRY(scratch_alloc(tp->s_mm, (size_t)n_tiles * d * 16, stream));
-  double* tmin = tp->s_mm.as<double>();
-  double* tmax = tmin + n_tiles * d;
+  const double* tmin = tminmax;
+  const double* tmax = tminmax ? tminmax + n_tiles * d : nullptr;
+  if (!tminmax) {
+    BM_TRY(scratch_alloc(tp->s_mm, (size_t)n_tiles * d * 16, stream));
+    tmin = tp->s_mm.as<double>();
+    tmax = tmin + n_tiles * d;
+  }
   BM_TRY(scratch_alloc(tp->s_cs, (size_t)(n_el * d + n_el) * 8, stream));
   double* center = tp->s_cs.as<double>();
   double* scale = center + n_el * d;
@@ -1161,12 +1182,23 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_te.ptr, 0, n_tiles * 8, stream));
 
   trace_mark("tc:prep start", stream);
-  tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(Xg, d, et, tp->d_tile_elem, n_tiles,
-                                                            tmin, tmax, cen);
-  BM_CHECK_LAUNCH();
-  elem_scale_kernel<<<(unsigned)n_el, 256, 0, stream>>>(d, et, tp->d_tbase, tmin, tmax, center,
-                                                        scale);
-  BM_CHECK_LAUNCH();
+  if (!tminmax) {
+    tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(
+        Xg, d, et, tp->d_tile_elem, n_tiles, const_cast<double*>(tmin), const_cast<double*>(tmax),
+        cen);
+    BM_CHECK_LAUNCH();
+  }
+  {
+    Scratch s_r;
+    BM_TRY(scratch_alloc(s_r, (size_t)n_el * 8, stream));
+    BM_CHECK_CUDA(cudaMemsetAsync(s_r.ptr, 0, n_el * 8, stream));
+    elem_center_kernel<<<dim3((unsigned)n_el, (unsigned)ceil_div(d, 32)), 256, 0, stream>>>(
+        d, et, tp->d_tbase, tmin, tmax, center, s_r.as<unsigned long long>());
+    BM_CHECK_LAUNCH();
+    elem_scale_kernel<<<(unsigned)ceil_div(n_el, 128), 128, 0, stream>>>(
+        n_el, s_r.as<unsigned long long>(), scale);
+    BM_CHECK_LAUNCH();
+  }
   if (rad) BM_CHECK_CUDA(cudaMemsetAsync(rad, 0, n_tiles * 8, stream));
   BM_TRY(scratch_alloc(tp->s_lim, (size_t)n_tiles * 8, stream));
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_lim.ptr, 0, n_tiles * 8, stream));

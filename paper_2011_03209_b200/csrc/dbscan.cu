@@ -932,6 +932,13 @@ __device__ __forceinline__ bool lunion(int* lp, int a, int b) {
   }
 }
 
+// one step of the in-warp 32x32 bit transpose: lane j ends with bit i = the
+// input word of lane i, bit j
+__device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32_t m, int lane) {
+  const uint32_t t = __shfl_xor_sync(0xffffffffu, w, s);
+  return (lane & s) ? ((w & ~m) | ((t >> s) & m)) : ((w & m) | ((t << s) & ~m));
+}
+
 template <bool DIAG>
 __global__ void __launch_bounds__(128)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
@@ -1056,14 +1063,32 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         }
         if (best < __ldcg(bmin + pI + r)) atomicMin(bmin + pI + r, best);
       }
-      // --- border: non-core column c -> its core row of smallest entry (off-diagonal only)
-      if (!DIAG && !cj && t < nk - J * kTile) {
-        const int c = t, wd = c >> 5, sh = c & 31;
-        int best = kNoCore;
-        for (int rr = 0; rr < kTile; ++rr)
-          if (((bits[rr * 4 + wd] >> sh) & 1u) && ((coreI[rr >> 5] >> (rr & 31)) & 1u))
-            best = min(best, et.ent[pI + rr]);
-        if (best < __ldcg(bmin + pJ + c)) atomicMin(bmin + pJ + c, best);
+      // --- border: non-core column c -> its core row of smallest entry
+      //     (off-diagonal only). Warp w owns columns 32w..32w+31 = word w: four
+      //     32x32 bit transposes give each lane its column's row bits, so only
+      //     the set bits are visited.
+      if (!DIAG) {
+        const bool need = !cj && t < nk - J * kTile;
+        if (__any_sync(0xffffffffu, need)) {  // warp-uniform
+          const int lane = t & 31, wd = t >> 5;
+          int best = kNoCore;
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb) {
+            uint32_t x = bits[(rb * 32 + lane) * 4 + wd];
+            x = bit_transpose_step(x, 16, 0x0000FFFFu, lane);
+            x = bit_transpose_step(x, 8, 0x00FF00FFu, lane);
+            x = bit_transpose_step(x, 4, 0x0F0F0F0Fu, lane);
+            x = bit_transpose_step(x, 2, 0x33333333u, lane);
+            x = bit_transpose_step(x, 1, 0x55555555u, lane);
+            uint32_t m = need ? (x & coreI[rb]) : 0u;  // bit i: row 32 rb + i, core
+            while (m) {
+              const int i = __ffs(m) - 1;
+              m &= m - 1;
+              best = min(best, et.ent[pI + rb * 32 + i]);
+            }
+          }
+          if (need && best < __ldcg(bmin + pJ + t)) atomicMin(bmin + pJ + t, best);
+        }
       }
       __syncthreads();
       // --- propagate local merges to the global forest

@@ -1033,8 +1033,11 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
           }
         }
       }
-      // --- core-core edges between nodes with different global roots
+      // --- core-core edges between nodes with different global roots; a row
+      //     joins each distinct neighbouring global root once (consecutive
+      //     bits mostly share the root, so `last` skips the repeats)
       if (ci && !uniform) {
+        int last = gr;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
@@ -1042,7 +1045,9 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
             const int c = w * 32 + __ffs(m) - 1;
             m &= m - 1;
             const int node = DIAG ? c : kTile + c;
-            if (groot[node] != gr) {
+            const int gn = groot[node];
+            if (gn != gr && (DIAG || gn != last)) {
+              last = gn;
               if (lunion(lp, r, node)) any_merge = 1;
             }
           }

@@ -15,7 +15,7 @@
 namespace bm {
 namespace {
 
-constexpr int kRChunk = 4096;
+constexpr int kRChunk = 1024;
 constexpr int kRBits = 8;
 constexpr int kRBins = 1 << kRBits;
 

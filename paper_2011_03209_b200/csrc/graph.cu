@@ -245,27 +245,38 @@ __global__ void node_stats_kernel(const double* __restrict__ X, int64_t d,
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n_nodes || c >= d) return;
   const int64_t a = node_off[v], b = node_off[v + 1];
+  // numpy axis-0 mean: the rows are added in order (an inherently serial
+  // fp64 chain); 32 row loads are in flight ahead of the dependent additions
   double s = 0.0;
-  for (int64_t i = a; i < b; ++i) s = __dadd_rn(s, X[node_rows[i] * d + c]);
+  int64_t i = a;
+  for (; i + 32 <= b; i += 32) {
+    double x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = X[node_rows[i + j] * d + c];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s = __dadd_rn(s, x[j]);
+  }
+  for (; i < b; ++i) s = __dadd_rn(s, X[node_rows[i] * d + c]);
   stats[v * d + c] = __ddiv_rn(s, (double)(b - a));
 }
 
-// numpy pairwise_sum (loops_utils.h.src) over f[rows[i] * m + ax], i < n:
-// a leaf of <= 128 terms uses 8 strided accumulators (plain loop below 8);
-// larger ranges split at n2 = n/2 - (n/2)%8. The recursion is emulated with an
-// explicit stack (device recursion overflows the per-thread stack for nodes
-// of ~100k rows).
-__device__ double pairwise_leaf(const double* __restrict__ f, int m, int ax,
-                                const int64_t* __restrict__ rows, int64_t n) {
+// numpy 1-D mean of the filter values of every node, in two parallel steps:
+// every pairwise-sum leaf (<= 128 rows, 8 strided accumulators) of every node
+// at once, then per node the leaf sums combined in the recursion's order
+// (leaf program built on the host from the node sizes).
+__device__ double pairwise_leaf_at(const double* __restrict__ f, int m, int ax,
+                                   const int64_t* __restrict__ rows, int64_t n) {
   if (n < 8) {
     double r = -0.0;
     for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, f[rows[i] * m + ax]);
     return r;
   }
   double r[8];
+#pragma unroll
   for (int j = 0; j < 8; ++j) r[j] = f[rows[j] * m + ax];
   int64_t i = 8;
   for (; i < n - (n % 8); i += 8)
+#pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f[rows[i + j] * m + ax]);
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -273,62 +284,43 @@ __device__ double pairwise_leaf(const double* __restrict__ f, int m, int ax,
   return res;
 }
 
-__device__ double pairwise_gather(const double* __restrict__ f, int m, int ax,
-                                  const int64_t* __restrict__ rows, int64_t n) {
-  if (n <= 128) return pairwise_leaf(f, m, ax, rows, n);
-  constexpr int kDepth = 48;  // n < 2^40
-  int64_t off_s[kDepth], n_s[kDepth];
-  double left_s[kDepth];
-  bool right_s[kDepth];  // false: left child pending, true: right child pending
-  int sp = 1;
-  off_s[0] = 0;
-  n_s[0] = n;
-  right_s[0] = false;
-  while (true) {
-    const int t = sp - 1;
-    const int64_t o = off_s[t], nn = n_s[t];
-    if (nn > 128) {  // fresh internal node: descend into its left half
-      int64_t n2 = nn / 2;
-      n2 -= n2 % 8;
-      off_s[sp] = o;
-      n_s[sp] = n2;
-      right_s[sp] = false;
-      ++sp;
-      continue;
-    }
-    double val = pairwise_leaf(f, m, ax, rows + o, nn);
-    --sp;
-    while (sp > 0) {  // hand the value to the parents
-      const int p = sp - 1;
-      if (!right_s[p]) {  // left half done: start the right half
-        left_s[p] = val;
-        right_s[p] = true;
-        int64_t n2 = n_s[p] / 2;
-        n2 -= n2 % 8;
-        off_s[sp] = off_s[p] + n2;
-        n_s[sp] = n_s[p] - n2;
-        right_s[sp] = false;
-        ++sp;
-        break;
-      }
-      val = __dadd_rn(left_s[p], val);  // left + right, as the recursion returns
-      --sp;
-    }
-    if (sp == 0) return val;
-  }
+struct NodeLeaf {
+  int64_t start;  // first entry of the leaf (absolute, into node_rows)
+  int32_t len, pops;
+};
+
+__global__ void node_leaf_kernel(const double* __restrict__ f, int m,
+                                 const int64_t* __restrict__ node_rows,
+                                 const NodeLeaf* __restrict__ leaves, int64_t n_leaves,
+                                 double* __restrict__ lsum) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_leaves * m) return;
+  const NodeLeaf L = leaves[t / m];
+  const int ax = (int)(t % m);
+  lsum[t] = pairwise_leaf_at(f, m, ax, node_rows + L.start, L.len);
 }
 
-__global__ void node_fmean_kernel(const double* __restrict__ f, int m,
-                                  const int64_t* __restrict__ node_rows,
-                                  const int64_t* __restrict__ node_off, int64_t n_nodes,
-                                  double* __restrict__ fmean) {
+__global__ void node_combine_kernel(const NodeLeaf* __restrict__ leaves,
+                                    const int64_t* __restrict__ leaf_off, int m,
+                                    const double* __restrict__ lsum,
+                                    const int64_t* __restrict__ node_off, int64_t n_nodes,
+                                    double* __restrict__ fmean) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_nodes * m) return;
   const int64_t v = t / m;
   const int ax = (int)(t % m);
-  const int64_t a = node_off[v], n = node_off[v + 1] - a;
-  double s = __dadd_rn(0.0, pairwise_gather(f, m, ax, node_rows + a, n));
-  fmean[t] = __ddiv_rn(s, (double)n);
+  constexpr int kS = 48;
+  double st[kS];
+  int sp = 0;
+  for (int64_t l = leaf_off[v]; l < leaf_off[v + 1]; ++l) {
+    st[sp++] = lsum[l * m + ax];
+    for (int q = 0; q < leaves[l].pops; ++q) {
+      st[sp - 2] = __dadd_rn(st[sp - 2], st[sp - 1]);
+      --sp;
+    }
+  }
+  const int64_t n = node_off[v + 1] - node_off[v];
+  fmean[t] = __ddiv_rn(__dadd_rn(0.0, sp > 0 ? st[0] : 0.0), (double)n);
 }
 
 inline unsigned grid1(int64_t n, int threads = 256) {
@@ -501,8 +493,35 @@ extern "C" int bm_node_stats(const double* d_X, int64_t d, const double* d_f, in
   }
   if (d_fmean) {
     BM_REQUIRE(d_f, "null filter values");
-    node_fmean_kernel<<<(unsigned)ceil_div(n_nodes * m, 64), 64, 0, s>>>(
-        d_f, m, d_node_rows, d_node_offsets, n_nodes, d_fmean);
+    // node sizes -> pairwise leaf programs (host), leaf sums and their
+    // combination (device)
+    std::vector<int64_t> off(n_nodes + 1);
+    BM_CHECK_CUDA(cudaMemcpyAsync(off.data(), d_node_offsets, (n_nodes + 1) * 8,
+                                  cudaMemcpyDeviceToHost, s));
+    BM_CHECK_CUDA(cudaStreamSynchronize(s));
+    std::vector<NodeLeaf> lv;
+    std::vector<int64_t> loff(n_nodes + 1, 0);
+    for (int64_t v = 0; v < n_nodes; ++v) {
+      const int64_t n = off[v + 1] - off[v];
+      BM_REQUIRE(n >= 1 && n < (1ll << 31), "bad node size");
+      for (const PwLeaf& L : pw_plan((int)n)) lv.push_back({off[v] + L.start, L.len, L.pops});
+      loff[v + 1] = (int64_t)lv.size();
+    }
+    const int64_t nl = (int64_t)lv.size();
+    Scratch sl, so, ss;
+    BM_TRY(scratch_alloc(sl, nl * sizeof(NodeLeaf), s));
+    BM_TRY(scratch_alloc(so, (n_nodes + 1) * 8, s));
+    BM_TRY(scratch_alloc(ss, (size_t)nl * m * 8, s));
+    BM_CHECK_CUDA(cudaMemcpyAsync(sl.ptr, lv.data(), nl * sizeof(NodeLeaf),
+                                  cudaMemcpyHostToDevice, s));
+    BM_CHECK_CUDA(cudaMemcpyAsync(so.ptr, loff.data(), (n_nodes + 1) * 8,
+                                  cudaMemcpyHostToDevice, s));
+    node_leaf_kernel<<<(unsigned)ceil_div(nl * m, 128), 128, 0, s>>>(
+        d_f, m, d_node_rows, sl.as<NodeLeaf>(), nl, ss.as<double>());
+    BM_CHECK_LAUNCH();
+    node_combine_kernel<<<(unsigned)ceil_div(n_nodes * m, 64), 64, 0, s>>>(
+        sl.as<NodeLeaf>(), so.as<int64_t>(), m, ss.as<double>(), d_node_offsets, n_nodes,
+        d_fmean);
     BM_CHECK_LAUNCH();
   }
   return BM_OK;

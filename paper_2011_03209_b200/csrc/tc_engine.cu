@@ -63,7 +63,6 @@ constexpr int kBM = 128;        // A rows (TMEM lanes)
 constexpr int kBN = 128;        // B rows per tile (MMA N)
 constexpr int kKC = 128;        // bytes per swizzle-128B row chunk
 constexpr int kStages = 2;      // B ring depth (full-K B tiles)
-constexpr int kUnitB = 32;      // B (= bitmap) tiles per work unit
 constexpr int kInfo = 3;        // per-tile info ring depth (smem)
 constexpr int kEpiWarps = 16;   // epilogue warps 4..19 (4 per TMEM lane quarter)
 constexpr int kEpiCols = kBN / (kEpiWarps / 4);  // columns per epilogue warp (32)
@@ -286,9 +285,6 @@ __device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32
   return (lane & s) ? ((w & ~m) | ((t >> s) & m)) : ((w & m) | ((t << s) & ~m));
 }
 
-__device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
   asm volatile(

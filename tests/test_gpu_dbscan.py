@@ -123,3 +123,39 @@ def test_cancel_check_is_polled():
         cluster_all(pc, [np.arange(50)], DbscanParams(0.5, 3), DistanceStrategy(),
                     cancel_check=cancel)
     assert calls
+
+
+@pytest.mark.parametrize("d", [5, 40, 300, 512, 600])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_grouped_pruned_elements_against_oracle(d, engine):
+    """Elements large enough for the spatial grouping and both pruning
+    bounds (several seed groups over well separated blobs), for the exact
+    engine at dims the tensor cores do not take (300, 512: pruning on; 600:
+    pruning off) and the tensor-core engine."""
+    from paper_2011_03209_b200 import DbscanParams, DistanceStrategy, cluster_all, from_array
+
+    X = O.gmm(2600, d, 6, 6.0, 50 + d)
+    eps = O.dist_quantile(X, 0.03, d)
+    rng = np.random.default_rng(d)
+    members = [np.sort(rng.choice(2600, s, replace=False)) for s in (2500, 1200, 400, 90)]
+    cl = cluster_all(from_array(X), members, DbscanParams(eps, 4),
+                     DistanceStrategy(threshold=10 ** 9), engine=engine)
+    for k, m in enumerate(members):
+        clusters, noise = O.dbscan_element(X, m, eps, 4, O.ORDER_SEQUENTIAL)
+        assert cl[k].clusters == clusters and cl[k].noise == noise, (d, k)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_nan_and_inf_rows(engine):
+    """Non-finite coordinates: scipy's distances are NaN/inf, never <= eps, so
+    those rows are noise; pruning and the tensor-core bounds must keep (not
+    prune or misclassify) every tile pair touching them."""
+    X = O.gmm(1500, 48, 4, 4.0, 9)
+    X[[3, 700, 701]] = np.nan
+    X[[40, 1200], 7] = np.inf
+    X[900, 2] = -np.inf
+    eps = O.dist_quantile(X[np.isfinite(X).all(axis=1)], 0.05, 9)
+    rows = np.arange(1500)
+    out = run(X, rows, eps, 4, order=O.ORDER_SEQUENTIAL, engine=engine)
+    clusters, noise = O.dbscan_element(X, rows, eps, 4, O.ORDER_SEQUENTIAL)
+    assert out.clusters == clusters and out.noise == noise

@@ -631,6 +631,10 @@ __global__ void emit_tiles_kernel(ElemTables et, const int32_t* __restrict__ row
   }
 }
 
+// tensor-core work units hold up to kTcUnit column tiles (the row tile's A
+// operand is loaded once per unit)
+constexpr int kTcUnit = 32;
+
 // unit counts per row tile (from the kept slots of consecutive rows)
 __global__ void unit_counts_kernel(const int64_t* __restrict__ row_first, int64_t n_rt,
                                    int64_t* __restrict__ n_off, int64_t* __restrict__ n_tc) {
@@ -638,7 +642,7 @@ __global__ void unit_counts_kernel(const int64_t* __restrict__ row_first, int64_
        rt += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = row_first[rt + 1] - row_first[rt];
     n_off[rt] = (c - 1 + 31) / 32;
-    n_tc[rt] = (c + 31) / 32;
+    n_tc[rt] = (c + kTcUnit - 1) / kTcUnit;
   }
 }
 
@@ -660,7 +664,8 @@ __global__ void emit_units_kernel(const int32_t* __restrict__ row_elem,
     int64_t o = off_pos[rt];
     for (int j = 1; j < c; j += 32) off[o++] = TileUnit{k, I, (int32_t)(f + j), min(32, c - j)};
     o = tc_pos[rt];
-    for (int j = 0; j < c; j += 32) tcu[o++] = TileUnit{k, I, (int32_t)(f + j), min(32, c - j)};
+    for (int j = 0; j < c; j += kTcUnit)
+      tcu[o++] = TileUnit{k, I, (int32_t)(f + j), min(kTcUnit, c - j)};
   }
 }
 

@@ -633,7 +633,7 @@ __global__ void emit_tiles_kernel(ElemTables et, const int32_t* __restrict__ row
 
 // tensor-core work units hold up to kTcUnit column tiles (the row tile's A
 // operand is loaded once per unit)
-constexpr int kTcUnit = 32;
+constexpr int kTcUnit = 16;
 
 // unit counts per row tile (from the kept slots of consecutive rows)
 __global__ void unit_counts_kernel(const int64_t* __restrict__ row_first, int64_t n_rt,

@@ -111,7 +111,8 @@ gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
 // first kGroupDims dims (fp32); a stable sort by (element, seed) makes row
 // tiles compact, so tile pairs of far-apart groups can be pruned.
 // ---------------------------------------------------------------------------
-constexpr int kGroupSeeds = 64;  // group_assign_kernel assumes 64 (two seeds per lane)
+constexpr int kGroupSeeds = 64;
+static_assert(kGroupSeeds == 64, "group_assign_kernel gives each lane two seeds (lane, lane + 32)");
 constexpr int kGroupDims = 32;
 constexpr int kGroupMinRows = 3 * kTile;  // smaller elements keep their order
 

@@ -14,7 +14,6 @@
 namespace bm {
 namespace {
 
-__constant__ PwProgram c_prog_lens;
 
 constexpr int kLensWarps = 8;
 
@@ -84,7 +83,8 @@ __device__ double warp_pairwise_row(const double* __restrict__ row, const PwProg
 }
 
 __global__ void __launch_bounds__(kLensWarps * 32)
-lens_l2_kernel(const double* __restrict__ X, int64_t n, int64_t d, double* __restrict__ out) {
+lens_l2_kernel(const double* __restrict__ X, int64_t n, int64_t d, double* __restrict__ out,
+               const __grid_constant__ PwProgram c_prog_lens) {
   __shared__ double s_leaf[kLensWarps][kMaxLeaves];
   const int warp = threadIdx.x >> 5;
   for (int64_t r = (int64_t)blockIdx.x * kLensWarps + warp; r < n;
@@ -189,12 +189,10 @@ __global__ void l2_apply_kernel(const double* __restrict__ X, int64_t n, int64_t
 int lens_l2(const double* X, int64_t n, int64_t d, double* out, cudaStream_t stream) {
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
-  BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(c_prog_lens, &prog, sizeof(prog), 0,
-                                        cudaMemcpyHostToDevice, stream));
   int64_t blocks = ceil_div(n, kLensWarps);
   int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  lens_l2_kernel<<<(unsigned)blocks, kLensWarps * 32, 0, stream>>>(X, n, d, out);
+  lens_l2_kernel<<<(unsigned)blocks, kLensWarps * 32, 0, stream>>>(X, n, d, out, prog);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }

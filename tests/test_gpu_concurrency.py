@@ -64,3 +64,39 @@ def test_concurrent_threads_match_sequential(engine):
     assert not errors, errors
     for (a, na), (b, nb) in zip(want, got):
         assert np.array_equal(a, b) and np.array_equal(na, nb)
+
+
+def test_concurrent_l2_lens_different_dims():
+    """The lens kernels' pairwise programs (one per d) are kernel arguments:
+    threads with different d on different streams stay bit-exact."""
+    import torch
+
+    from paper_2011_03209_b200 import engine as eng
+    from paper_2011_03209_b200.device import require_gpu, to_device_f64
+
+    dev = require_gpu()
+    rng = np.random.default_rng(0)
+    mats = [rng.standard_normal((20000, d)) for d in (3, 130, 257, 1000)]
+    want = [O.lens(X, "l2-norm") for X in mats]
+    got = [None] * len(mats)
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                Xd = to_device_f64(mats[i], dev)
+                for _ in range(5):
+                    got[i] = eng.lens(Xd, 1).cpu().numpy()
+                s.synchronize()
+        except Exception as e:
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(len(mats))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for a, b in zip(want, got):
+        assert np.array_equal(a, b)

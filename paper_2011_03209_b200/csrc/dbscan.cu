@@ -206,13 +206,19 @@ group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int e = it.e0 + (threadIdx.x >> 5); e < it.e1; e += blockDim.x >> 5) {
-    const double* x = X + rows[e] * d;
-    const float x0 = lane < D ? (float)x[lane] : 0.0f;
-    const float x1 = lane + 32 < D ? (float)x[lane + 32] : 0.0f;
-    float d0 = 0.0f, d1 = 0.0f;  // seeds lane, lane + 32
-    for (int dim = 0; dim < D; ++dim) {
-      const float xv = __shfl_sync(0xffffffffu, dim < 32 ? x0 : x1, dim & 31);
+  static_assert(kGroupDims <= 32, "one dim per lane");
+  const int nw = blockDim.x >> 5;
+  int e = it.e0 + (threadIdx.x >> 5);
+  // the next entry's coordinates are loaded while the current one is scored
+  float xn = (e < it.e1 && lane < D) ? (float)X[rows[e] * d + lane] : 0.0f;
+  for (; e < it.e1; e += nw) {
+    const float x0 = xn;
+    const int en = e + nw;
+    xn = (en < it.e1 && lane < D) ? (float)X[rows[en] * d + lane] : 0.0f;
+    float d0 = 0.0f, d1 = 0.0f;  // seeds lane, lane + 32 (dims >= D are 0 on both sides)
+#pragma unroll
+    for (int dim = 0; dim < kGroupDims; ++dim) {
+      const float xv = __shfl_sync(0xffffffffu, x0, dim);
       const float a = xv - sd[dim][lane], b = xv - sd[dim][lane + 32];
       d0 = fmaf(a, a, d0);
       d1 = fmaf(b, b, d1);

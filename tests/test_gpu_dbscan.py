@@ -159,3 +159,33 @@ def test_nan_and_inf_rows(engine):
     out = run(X, rows, eps, 4, order=O.ORDER_SEQUENTIAL, engine=engine)
     clusters, noise = O.dbscan_element(X, rows, eps, 4, O.ORDER_SEQUENTIAL)
     assert out.clusters == clusters and out.noise == noise
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("case", ["identical", "tiny_eps", "huge_eps", "duplicates", "one_dim_line"])
+def test_degenerate_inputs(engine, case):
+    """Degenerate geometry on both engines (and through the grouping/pruning
+    path): zero spread, every pair in or out, duplicated rows, collinear data."""
+    rng = np.random.default_rng(5)
+    n, d = 900, 64
+    if case == "identical":
+        X, eps = np.full((n, d), 3.25), 0.5
+    elif case == "tiny_eps":
+        X = O.gmm(n, d, 3, 3.0, 5)
+        eps = 1e-9
+    elif case == "huge_eps":
+        X = O.gmm(n, d, 3, 3.0, 5)
+        eps = 1e6
+    elif case == "duplicates":
+        base = O.gmm(300, d, 3, 3.0, 5)
+        X = base[rng.integers(0, 300, n)]
+        eps = O.dist_quantile(base, 0.01, 5)
+    else:
+        t = np.sort(rng.uniform(0, 100, n))
+        X = np.outer(t, np.ones(d) / np.sqrt(d))
+        eps = 0.3
+    rows = np.arange(n)
+    for order in (O.ORDER_SEQUENTIAL, O.ORDER_PAIRWISE):
+        out = run(X, rows, eps, 4, order=order, engine=engine)
+        clusters, noise = O.dbscan_element(X, rows, eps, 4, order)
+        assert out.clusters == clusters and out.noise == noise, (case, order)

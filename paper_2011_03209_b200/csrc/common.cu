@@ -108,7 +108,78 @@ int device_free_bytes(size_t* free_b) {
   return BM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Cached large buffers (see BigScratch): mapping tens of GB through the
+// stream-ordered pool costs ~60 ms per GB whenever the pool cannot reuse one
+// contiguous block, so the bitmap of a huge element is kept between calls.
+// ---------------------------------------------------------------------------
+namespace {
+struct BigBuf {
+  void* p;
+  size_t bytes;
+  int dev;
+  bool busy;
+};
+std::mutex g_big_mu;
+std::vector<BigBuf> g_big;
+}  // namespace
+
+int big_acquire(size_t bytes, void** out, int* slot) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  int best = -1;
+  for (int i = 0; i < (int)g_big.size(); ++i) {
+    const BigBuf& b = g_big[i];
+    if (!b.busy && b.dev == dev && b.bytes >= bytes && (best < 0 || b.bytes < g_big[best].bytes))
+      best = i;
+  }
+  if (best < 0) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {  // give back the idle cached buffers and retry once
+      cudaGetLastError();
+      for (auto& b : g_big)
+        if (!b.busy && b.dev == dev && b.p) {
+          cudaFree(b.p);
+          b.p = nullptr;
+          b.bytes = 0;
+        }
+      e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+      return BM_ERR_NOMEM;
+    }
+    g_big.push_back({p, bytes, dev, false});
+    best = (int)g_big.size() - 1;
+  }
+  g_big[best].busy = true;
+  *out = g_big[best].p;
+  *slot = best;
+  return BM_OK;
+}
+
+void big_release(int slot) {
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  if (slot >= 0 && slot < (int)g_big.size()) g_big[slot].busy = false;
+}
+
+void big_trim() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  for (auto& b : g_big)
+    if (!b.busy && b.dev == dev && b.p) {
+      cudaFree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+    }
+}
+
 void release_pool() {
+  big_trim();
   int dev = 0;
   cudaGetDevice(&dev);
   cudaMemPool_t pool;

@@ -86,6 +86,33 @@ int sort_pairs_u64(uint64_t* keys, int64_t* vals, int64_t n, int key_bits, cudaS
 void trace_mark(const char* name, cudaStream_t s);
 void trace_dump();
 
+// A large buffer kept across calls (cudaMalloc'd once per size class, reused
+// by later calls; bm_release_scratch frees the idle ones). The holder must not
+// release it before the stream's work on it has completed.
+int big_acquire(size_t bytes, void** out, int* slot);
+void big_release(int slot);
+struct BigScratch {
+  void* ptr = nullptr;
+  int slot = -1;
+  cudaStream_t stream = nullptr;  // work on the buffer is drained before release
+  BigScratch() = default;
+  BigScratch(const BigScratch&) = delete;
+  BigScratch& operator=(const BigScratch&) = delete;
+  ~BigScratch() {
+    if (slot >= 0 && stream) cudaStreamSynchronize(stream);
+    big_release(slot);
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+inline int big_scratch(BigScratch& b, size_t bytes, cudaStream_t stream) {
+  if (b.slot >= 0 && b.stream) cudaStreamSynchronize(b.stream);
+  big_release(b.slot);
+  b.slot = -1;
+  b.stream = stream;
+  return big_acquire(bytes, &b.ptr, &b.slot);
+}
+
 // Free device memory including what the stream-ordered pool retains unused.
 int device_free_bytes(size_t* free_b);
 

@@ -1884,8 +1884,10 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       }
       size_t max_w = 0;
       for (auto& w : wins) max_w = std::max(max_w, bc.window_bytes(w.first, w.second));
-      Scratch adj;
-      BM_TRY(scratch_alloc(adj, max_w, stream));
+      // the bitmap: a cached buffer (released after finish() synchronised)
+      BigScratch adj;
+      BM_TRY(big_scratch(adj, max_w, stream));
+      trace_mark("batch:bitmap allocated", stream);
       BM_CHECK_CUDA(cudaEventRecord(ev0, stream));
       // pass 1: counts of every window (the last window's bits stay resident);
       // pass 2: components of the resident window, then of the others with

@@ -1293,9 +1293,11 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     attr = true;
   }
   BM_TRY(scratch_alloc(s_tt, (size_t)n_tiles * sizeof(TileThr), stream));
+  trace_mark("tc:thr allocated", stream);
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
     BM_TRY(scratch_alloc(s_q, qcap * sizeof(int4), stream));
+    trace_mark("tc:queue allocated", stream);
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(nonempty, 0, (size_t)n_tiles * 4, stream));

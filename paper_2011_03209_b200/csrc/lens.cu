@@ -82,11 +82,62 @@ __device__ double warp_pairwise_row(const double* __restrict__ row, const PwProg
   return __shfl_sync(0xffffffffu, total, 0);
 }
 
+// Packed form for rows of 1, 2 or 4 full leaves (8 <= d <= 512 with every
+// leaf >= 8 long): the 4 lane groups of a warp cover 4 / n_leaves rows at
+// once, each lane loads its (<= 16) strided values of the leaf up front, and
+// the leader of each row replays the leaf program. Same additions, same order
+// as warp_pairwise_row.
+__device__ __forceinline__ double packed_leaf(const double* __restrict__ row, int start, int len,
+                                              int j) {
+  double v[16];
+  const int body = len - (len % 8);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (8 * i < body) ? __ldg(row + start + 8 * i + j) : 0.0;
+  double r = __dmul_rn(v[0], v[0]);
+#pragma unroll
+  for (int i = 1; i < 16; ++i)
+    if (8 * i < body) r = __dadd_rn(r, __dmul_rn(v[i], v[i]));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  for (int i = body; i < len; ++i) {
+    const double t = row[start + i];
+    r = __dadd_rn(r, __dmul_rn(t, t));
+  }
+  return r;
+}
+
 __global__ void __launch_bounds__(kLensWarps * 32)
 lens_l2_kernel(const double* __restrict__ X, int64_t n, int64_t d, double* __restrict__ out,
-               const __grid_constant__ PwProgram c_prog_lens) {
+               const __grid_constant__ PwProgram c_prog_lens, int packed) {
   __shared__ double s_leaf[kLensWarps][kMaxLeaves];
   const int warp = threadIdx.x >> 5;
+  if (packed) {
+    const int nl = c_prog_lens.n_leaves, rpw = 4 / nl;
+    const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+    const int sub = g / nl, li = g % nl;
+    const PwLeaf L = c_prog_lens.leaf[li];
+    for (int64_t r0 = ((int64_t)blockIdx.x * kLensWarps + warp) * rpw; r0 < n;
+         r0 += (int64_t)gridDim.x * kLensWarps * rpw) {
+      const int64_t r = min(r0 + sub, n - 1);  // tail: duplicate work, not stored
+      const double v = packed_leaf(X + r * d, L.start, L.len, j);
+      if (j == 0) s_leaf[warp][g] = v;
+      __syncwarp();
+      if (j == 0 && li == 0 && r0 + sub < n) {
+        PwStack st;
+#pragma unroll
+        for (int i = 0; i < kMaxStack; ++i) st.s[i] = 0.0;
+        for (int k = 0; k < nl; ++k) {
+          st.push(s_leaf[warp][g + k]);
+          for (int p = 0; p < c_prog_lens.leaf[k].pops; ++p) st.reduce();
+        }
+        // reduction result = identity(+0.0) + pairwise(...)
+        out[r0 + sub] = __dsqrt_rn(__dadd_rn(0.0, st.s[0]));
+      }
+      __syncwarp();
+    }
+    return;
+  }
   for (int64_t r = (int64_t)blockIdx.x * kLensWarps + warp; r < n;
        r += (int64_t)gridDim.x * kLensWarps) {
     double s = warp_pairwise_row<true>(X + r * d, c_prog_lens, s_leaf[warp]);
@@ -189,10 +240,13 @@ __global__ void l2_apply_kernel(const double* __restrict__ X, int64_t n, int64_t
 int lens_l2(const double* X, int64_t n, int64_t d, double* out, cudaStream_t stream) {
   PwProgram prog;
   BM_TRY(make_pw_program(d, &prog));
-  int64_t blocks = ceil_div(n, kLensWarps);
-  int64_t cap = (int64_t)num_sms() * 16;
+  int packed = prog.n_leaves == 1 || prog.n_leaves == 2 || prog.n_leaves == 4;
+  for (int i = 0; i < prog.n_leaves; ++i) packed &= prog.leaf[i].len >= 8 && prog.leaf[i].len <= 135;
+  const int rpw = packed ? 4 / prog.n_leaves : 1;
+  int64_t blocks = ceil_div(ceil_div(n, rpw), kLensWarps);
+  int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  lens_l2_kernel<<<(unsigned)blocks, kLensWarps * 32, 0, stream>>>(X, n, d, out, prog);
+  lens_l2_kernel<<<(unsigned)blocks, kLensWarps * 32, 0, stream>>>(X, n, d, out, prog, packed);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }

@@ -23,8 +23,8 @@ def _dev(x, dev):
     return to_device_f64(x, dev)
 
 
-@pytest.mark.parametrize("d", [1, 2, 3, 7, 8, 9, 31, 64, 100, 128, 129, 200, 256, 257, 384, 512,
-                               1000, 2048])
+@pytest.mark.parametrize("d", [1, 2, 3, 7, 8, 9, 15, 16, 31, 64, 100, 128, 129, 136, 200, 250, 256,
+                               257, 264, 384, 500, 512, 1000, 2048])
 def test_lens_bit_exact(dev, d):
     from paper_2011_03209_b200 import engine, _native
 
@@ -38,6 +38,18 @@ def test_lens_bit_exact(dev, d):
     assert np.array_equal(engine.lens(Xd, _native.LENS_LINF).cpu().numpy(),
                           np.abs(X).max(axis=1))
     assert np.array_equal(engine.lens(Xd, _native.LENS_COLUMN, d - 1).cpu().numpy(), X[:, d - 1])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+@pytest.mark.parametrize("d", [64, 256, 512])
+def test_lens_few_rows(dev, n, d):
+    """Rows packed 4 / 2 / 1 per warp: the tail of a row count not divisible
+    by the packing must be written exactly once."""
+    from paper_2011_03209_b200 import engine, _native
+
+    X = np.random.default_rng(n * d).standard_normal((n, d))
+    assert np.array_equal(engine.lens(_dev(X, dev), _native.LENS_L2).cpu().numpy(),
+                          np.sqrt((X ** 2).sum(axis=1)))
 
 
 def test_lens_large_rows(dev):

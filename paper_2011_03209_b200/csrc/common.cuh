@@ -123,6 +123,20 @@ int num_sms();
 // Total memory of the current device (cached per device).
 size_t device_total_bytes();
 
+// fp64 -> fp32 rounding toward zero in integer ops, for |x| in the normal
+// fp32 range or x == +-0 (*ok true); other inputs leave *ok false and need
+// the conversion instruction. sm_100's fp64 conversions run on a narrow unit
+// (~2 per clock per SM), so bulk conversions go through here. Relative error
+// < 2^-23.
+__device__ __forceinline__ float f64_to_f32_rz(double x, bool* ok) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const unsigned hi = (unsigned)(b >> 32);
+  const unsigned e = (hi >> 20) & 0x7ffu;
+  *ok = (e - 897u <= 253u) || (b << 1) == 0;
+  const unsigned m = (unsigned)(b >> 29) & 0x7fffffu;
+  return __uint_as_float((hi & 0x80000000u) | (e ? ((e - 896u) << 23) | m : 0u));
+}
+
 // ---------------------------------------------------------------------------
 // Device-wide exclusive scan over int64 (in-place allowed). n may be 0.
 // ---------------------------------------------------------------------------

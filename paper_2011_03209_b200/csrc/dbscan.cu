@@ -363,7 +363,7 @@ constexpr int kProjKC = 16;  // dims staged per step (register-prefetched)
 
 // one CTA per grouped row tile: D[x][g] = <x, s_g> for its 128 rows and the 64
 // seeds (fp32, 4 x 8 per thread), then proj[rt][g] = min_x (D[x][a] - D[x][g])
-// minus the rounding bound (d + 2) 2^-23 (|c_T| + r_T)(|s_a| + |s_g|)
+// minus the rounding bound (d + 4) 2^-23 (|c_T| + r_T)(|s_a| + |s_g|)
 __global__ void __launch_bounds__(256, 3)
 tile_project_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, int64_t n_rt,
                     const int32_t* __restrict__ tseed, const float* __restrict__ sf,
@@ -414,10 +414,22 @@ tile_project_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, int
     }
   };
   auto stage = [&]() {
+    bool all_ok = true;
+    float xf[kXv];
+#pragma unroll
+    for (int u = 0; u < kXv; ++u) {
+      bool ok;
+      xf[u] = f64_to_f32_rz(xr[u], &ok);
+      all_ok &= ok;
+    }
+    if (!__all_sync(0xffffffffu, all_ok)) {  // rare: outside the fp32 normal range
+#pragma unroll
+      for (int u = 0; u < kXv; ++u) xf[u] = (float)xr[u];
+    }
 #pragma unroll
     for (int u = 0; u < kXv; ++u) {
       const int i = t + u * 256;
-      xs[i % kProjKC][i / kProjKC] = (float)xr[u];
+      xs[i % kProjKC][i / kProjKC] = xf[u];
     }
 #pragma unroll
     for (int u = 0; u < kSv; ++u) {
@@ -460,8 +472,9 @@ tile_project_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, int
     float m = 3.0e38f;
     for (int pnt = 0; pnt < valid; ++pnt) m = fminf(m, dd[pnt][a] - dd[pnt][t]);
     // |fl(<x,s>) - <x,s>| <= (d+2) 2^-24 |x||s| for the fp32 inputs and FMA
-    // chain; doubled for the input rounding of x and s, and the difference of
-    // two dots is rounded once more (absorbed by the +2)
+    // chain; x is rounded toward zero (2^-23) and s to nearest (2^-24), and
+    // the difference of two dots is rounded once more: (d+6) 2^-24 in all,
+    // below the (2d+8) 2^-24 used
     const double xmax = (cn + rad[rt]) * (1.0 + 1e-12);
     const double err = ((double)d + 4.0) * 1.1920928955078125e-07 * xmax *
                        (snorm[(int64_t)k * kGroupSeeds + a] + snorm[(int64_t)k * kGroupSeeds + t]) *

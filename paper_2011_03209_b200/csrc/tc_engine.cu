@@ -781,38 +781,169 @@ __global__ void elem_scale_kernel(int64_t n_el, const unsigned long long* __rest
   scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
 }
 
-// one warp per padded row: limbs into the three planes (4 columns per lane,
-// packed 32-bit stores), N = sum q^2 (exact), e = |x - c - s q| (fp64) -> tile
-// max via atomicMax on the bit pattern; with cen != null also the row's
-// distance to its tile centre -> tile radius (raw max, NaN-propagating)
-__global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad,
-                                ElemTables et, int64_t P, const double* __restrict__ center,
-                                const double* __restrict__ scale, int8_t* __restrict__ planes,
-                                int64_t* __restrict__ nq, int32_t* __restrict__ cq,
-                                unsigned long long* __restrict__ tile_e,
-                                const double* __restrict__ cen,
-                                unsigned long long* __restrict__ rad_bits,
-                                uint32_t* __restrict__ limb_sq) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t p = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); p < P;
-       p += (int64_t)gridDim.x * wpb) {
-    int64_t a = 0, bb = et.n_el;
-    while (bb - a > 1) {
-      int64_t mid = (a + bb) >> 1;
-      if (et.pbase[mid] <= p) a = mid; else bb = mid;
+// one block per tile, one warp per padded row: limbs into the three planes (4
+// columns per lane, packed 32-bit stores), N = sum q^2 (exact),
+// e = |x - c - s q| (fp64) -> tile max (bit pattern, one atomicMax per tile);
+// with cen != null also the row's distance to its tile centre -> tile radius
+// (raw max, NaN-propagating).
+// BULK: the block's rows stream through a shared-memory ring of kQRows-row
+// stages filled by cp.async.bulk (a tile is 128 contiguous rows of Xg), so
+// tens of KB per SM are in flight instead of one register load per lane.
+constexpr int kQWarps = 8;  // blockDim.x == 256
+constexpr int kQRows = kQWarps;  // rows per ring stage (one per warp)
+constexpr int kQIters = kTile / kQRows;
+constexpr int kQMaxStages = 4;
+constexpr int kQSmem = 96 * 1024;  // ring budget
+
+template <bool BULK>
+__global__ void __launch_bounds__(256)
+quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTables et, int64_t P,
+                const double* __restrict__ center, const double* __restrict__ scale,
+                int8_t* __restrict__ planes, int64_t* __restrict__ nq, int32_t* __restrict__ cq,
+                unsigned long long* __restrict__ tile_e, const double* __restrict__ cen,
+                unsigned long long* __restrict__ rad_bits, uint32_t* __restrict__ limb_sq,
+                int n_stages) {
+  extern __shared__ __align__(128) double q_ring[];
+  __shared__ __align__(8) uint64_t q_full[kQMaxStages];
+  __shared__ unsigned long long s_red[5][kQWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n_tiles = P / kTile;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t n_it = my_tiles * kQIters;
+  const uint32_t stage_bytes = (uint32_t)(kQRows * d * 8);
+  auto issue = [&](int64_t i, int sl) {  // iteration i into ring slot sl
+    const int64_t row0 = (blockIdx.x + (i / kQIters) * gridDim.x) * kTile + (i % kQIters) * kQRows;
+    uint64_t* bar = q_full + sl;
+    mbar_expect_tx(bar, stage_bytes);
+    bulk_load(q_ring + sl * kQRows * d, Xg + row0 * d, stage_bytes, bar);
+  };
+  if (BULK) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < n_stages; ++i) mbar_init(q_full + i, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int i = 0; i < n_stages && i < n_it; ++i) issue(i, i);
     }
-    const int k = (int)a;
+    __syncthreads();
+  }
+  int k = 0;
+  double sc = 1.0, inv = 1.0;
+  // per-warp maxima over its rows (lane 0): |M|^2, |L|^2 and the bit patterns
+  // of the squared error / |x - c|^2 / radius sums (square roots per tile)
+  unsigned long long w_m = 0, w_l = 0, w_e = 0, w_y = 0, w_r = 0;
+  bool w_valid = false;
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t t = blockIdx.x;
+  int sub = 0;  // row group within the tile
+  for (int64_t i = 0; i < n_it; ++i) {
+    if (sub == 0) {
+      int64_t a = 0, bb = et.n_el;
+      while (bb - a > 1) {
+        int64_t mid = (a + bb) >> 1;
+        if (et.pbase[mid] <= t * kTile) a = mid; else bb = mid;
+      }
+      k = (int)a;  // tiles never straddle elements
+      sc = scale[k];
+      inv = 1.0 / sc;
+      w_m = w_l = w_e = w_y = w_r = 0;
+      w_valid = false;
+      if (BULK) {  // the element centre and the tile centre, once per tile
+        double* s_c = q_ring + n_stages * kQRows * d;
+        for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+          s_c[c] = center[(int64_t)k * d + c];
+          s_c[d + c] = cen ? cen[t * d + c] : 0.0;
+        }
+        __syncthreads();
+      }
+    }
+    const int64_t p = t * kTile + sub * kQRows + warp;
+    const double* xr;
+    if (BULK) {
+      mbar_wait(q_full + slot, phase);
+      xr = q_ring + slot * kQRows * d + warp * d;
+    } else {
+      xr = Xg + p * d;
+    }
     const bool valid = (p - et.pbase[k]) < et.nrows[k];
-    const double s = scale[k];
-    const double inv = 1.0 / s;
-    const double* xr = Xg + p * d;
-    const double* ck = center + (int64_t)k * d;
-    const double* ct = cen ? cen + (p / kTile) * d : nullptr;
+    const double* ck = BULK ? q_ring + n_stages * kQRows * d : center + (int64_t)k * d;
+    const double* ct = cen ? (BULK ? ck + d : cen + t * d) : nullptr;
     long long nsum = 0;
     uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
     double esum = 0.0, ysum = 0.0, rsum = 0.0;
+    int8_t* const hrow = planes + p * kpad;
+    int8_t* const mrow = planes + P * kpad + p * kpad;
+    int8_t* const lrow = planes + 2 * P * kpad + p * kpad;
+    // Fast path (full 4-column groups of a valid row): rint and the integer
+    // conversion by the 1.5 * 2^52 trick (exact rint, ties to even, for
+    // |v| < 2^51), byte packing with PRMT, limb norms with DP4A, sum q^2 in
+    // fp64 (per lane <= 256 * 2^42 < 2^53: exact). A row with any
+    // |v| >= qmax (clamping, inf, NaN) is redone by the generic path.
+    constexpr double kMagic = 6755399441055744.0;
+    constexpr double kQMax = (double)((1 << kQBits) - 1);
+    bool bad = false;
+    double nsd = 0.0;
+    if (valid) {
+      for (int64_t c4 = 4 * lane; c4 < kpad && c4 + 4 <= d; c4 += 128) {
+        double xv[4], cv[4], tv[4];
+        if (BULK && (d & 1) == 0) {  // shared memory, 16-byte aligned
+          const double2 u0 = *reinterpret_cast<const double2*>(xr + c4);
+          const double2 u1 = *reinterpret_cast<const double2*>(xr + c4 + 2);
+          xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
+          const double2 c0 = *reinterpret_cast<const double2*>(ck + c4);
+          const double2 c1 = *reinterpret_cast<const double2*>(ck + c4 + 2);
+          cv[0] = c0.x, cv[1] = c0.y, cv[2] = c1.x, cv[3] = c1.y;
+          if (ct) {
+            const double2 t0 = *reinterpret_cast<const double2*>(ct + c4);
+            const double2 t1 = *reinterpret_cast<const double2*>(ct + c4 + 2);
+            tv[0] = t0.x, tv[1] = t0.y, tv[2] = t1.x, tv[3] = t1.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            xv[j] = xr[c4 + j];
+            cv[j] = ck[c4 + j];
+            tv[j] = ct ? ct[c4 + j] : 0.0;
+          }
+        }
+        int q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double y = xv[j] - cv[j];
+          const double v = y * inv;
+          bad |= !(fabs(v) < kQMax);
+          const double tq = __dadd_rn(v, kMagic);
+          const double qd = __dsub_rn(tq, kMagic);
+          q[j] = __double2loint(tq);
+          const double e = y - qd * sc;
+          esum += e * e;
+          ysum += y * y;
+          nsd = fma(qd, qd, nsd);
+          if (ct) {
+            const double dr = xv[j] - tv[j];
+            rsum += dr * dr;
+          }
+        }
+        const uint32_t lw = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
+                                        __byte_perm(q[2], q[3], 0x0040), 0x5410) & 0x7f7f7f7fu;
+        const uint32_t mw = __byte_perm(__byte_perm(q[0] >> kLimb, q[1] >> kLimb, 0x0040),
+                                        __byte_perm(q[2] >> kLimb, q[3] >> kLimb, 0x0040),
+                                        0x5410) & 0x7f7f7f7fu;
+        const uint32_t hw = __byte_perm(
+            __byte_perm(q[0] >> (2 * kLimb), q[1] >> (2 * kLimb), 0x0040),
+            __byte_perm(q[2] >> (2 * kLimb), q[3] >> (2 * kLimb), 0x0040), 0x5410);
+        msq = __dp4a(mw, mw, msq);
+        lsq = __dp4a(lw, lw, lsq);
+        *reinterpret_cast<uint32_t*>(hrow + c4) = hw;
+        *reinterpret_cast<uint32_t*>(mrow + c4) = mw;
+        *reinterpret_cast<uint32_t*>(lrow + c4) = lw;
+      }
+    }
+    nsum = (long long)nsd;
+    const bool redo = __any_sync(0xffffffffu, bad);
+    if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
+    // generic path: the tail columns (or the whole row when redo / padding)
     for (int64_t c4 = 4 * lane; c4 < kpad; c4 += 128) {
+      if (!redo && valid && c4 + 4 <= d) continue;
       uint32_t hw = 0, mw = 0, lw = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -822,9 +953,9 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
           const double x = xr[c];
           const double y = x - ck[c];
           double qd = rint(y * inv);
-          qd = fmin(fmax(qd, -(double)((1 << kQBits) - 1)), (double)((1 << kQBits) - 1));
+          qd = fmin(fmax(qd, -kQMax), kQMax);
           q = (int)qd;
-          const double e = y - qd * s;
+          const double e = y - qd * sc;
           esum += e * e;
           ysum += y * y;
           if (ct) {
@@ -837,37 +968,96 @@ __global__ void quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_
         msq += mq * mq;
         lsq += lq * lq;
         hw |= (uint32_t)(uint8_t)(int8_t)(q >> (2 * kLimb)) << (8 * j);
-        mw |= (uint32_t)((q >> kLimb) & ((1 << kLimb) - 1)) << (8 * j);
-        lw |= (uint32_t)(q & ((1 << kLimb) - 1)) << (8 * j);
+        mw |= mq << (8 * j);
+        lw |= lq << (8 * j);
       }
-      *reinterpret_cast<uint32_t*>(planes + p * kpad + c4) = hw;
-      *reinterpret_cast<uint32_t*>(planes + P * kpad + p * kpad + c4) = mw;
-      *reinterpret_cast<uint32_t*>(planes + 2 * P * kpad + p * kpad + c4) = lw;
+      *reinterpret_cast<uint32_t*>(hrow + c4) = hw;
+      *reinterpret_cast<uint32_t*>(mrow + c4) = mw;
+      *reinterpret_cast<uint32_t*>(lrow + c4) = lw;
+    }
+    if (BULK) {
+      // every warp is done with this stage: refill it
+      __syncthreads();
+      if (threadIdx.x == 0 && i + n_stages < n_it) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(i + n_stages, slot);
+      }
+      if (++slot == n_stages) slot = 0, phase ^= 1u;
+    }
+    // row sums: 32-bit limb norms by REDUX; sum q^2 (< 2^63) in three 21-bit
+    // chunks by REDUX; the fp64 sums by shuffles
+    msq = __reduce_add_sync(0xffffffffu, msq);
+    lsq = __reduce_add_sync(0xffffffffu, lsq);
+    {
+      const unsigned long long u = (unsigned long long)nsum;  // per lane < 2^55
+      const unsigned long long c0 = __reduce_add_sync(0xffffffffu, (unsigned)(u & 0x1fffff));
+      const unsigned long long c1 =
+          __reduce_add_sync(0xffffffffu, (unsigned)((u >> 21) & 0x1fffff));
+      const unsigned long long c2 = __reduce_add_sync(0xffffffffu, (unsigned)(u >> 42));
+      nsum = (long long)(c0 + (c1 << 21) + (c2 << 42));
     }
     for (int o = 16; o; o >>= 1) {
-      nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       esum += __shfl_xor_sync(0xffffffffu, esum, o);
       ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
       rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-      msq += __shfl_xor_sync(0xffffffffu, msq, o);
-      lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
     }
     if (lane == 0) {
       nq[p] = nsum;
       cq[p] = (int32_t)(nsum >> kYShift);
-      atomicMax(limb_sq + 2 * (p / kTile), msq);  // pads are all-zero rows
-      atomicMax(limb_sq + 2 * (p / kTile) + 1, lsq);
+      w_m = max(w_m, (unsigned long long)msq);  // pads are all-zero rows
+      w_l = max(w_l, (unsigned long long)lsq);
       if (valid) {
-        // rigorous upper bound of |x - c - s q|: the fp64 evaluation of each
-        // coordinate of e is off by <= 3.1u|y_k| (u = 2^-53), so add 1e-15|y|
-        const double e = sqrt(esum) * (1.0 + 1e-12) + 1e-15 * sqrt(ysum) + 1e-300;
-        atomicMax(tile_e + p / kTile, (unsigned long long)__double_as_longlong(e));
-        if (rad_bits) {
-          const double rr = sqrt(rsum);  // NaN (positive) sorts above every finite value
-          atomicMax(rad_bits + p / kTile,
-                    (unsigned long long)__double_as_longlong(rr == rr ? rr : __longlong_as_double(0x7ff8000000000000ll)));
+        // NaN (any sign) -> the positive quiet NaN, above every finite value
+        auto bits = [](double v) {
+          return (unsigned long long)__double_as_longlong(
+              v == v ? v : __longlong_as_double(0x7ff8000000000000ll));
+        };
+        w_e = max(w_e, bits(esum));
+        w_y = max(w_y, bits(ysum));
+        w_r = max(w_r, bits(rsum));
+        w_valid = true;
+      }
+    }
+    if (++sub == kQIters) {
+      // tile maxima: one atomic per tile and array (the arrays start zeroed).
+      // sqrt is monotonic, so the tile's error bound
+      //   sqrt(max esum) (1 + 1e-12) + 1e-15 sqrt(max ysum) + 1e-300
+      // bounds every row's |x - c - s q| (the fp64 evaluation of each
+      // coordinate of e is off by <= 3.1u|y_k|, u = 2^-53), and
+      // sqrt(max rsum) is the max row distance to the tile centre.
+      if (lane == 0) {
+        s_red[0][warp] = w_m, s_red[1][warp] = w_l;
+        s_red[2][warp] = w_valid ? w_e + 1 : 0;  // +1: nonzero marks "has valid rows"
+        s_red[3][warp] = w_y;
+        s_red[4][warp] = w_r;
+      }
+      __syncthreads();
+      if (threadIdx.x < 5) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < kQWarps; ++w) m = max(m, s_red[threadIdx.x][w]);
+        s_red[threadIdx.x][0] = m;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        atomicMax(limb_sq + 2 * t, (uint32_t)s_red[0][0]);
+        atomicMax(limb_sq + 2 * t + 1, (uint32_t)s_red[1][0]);
+        if (s_red[2][0]) {
+          const double es = __longlong_as_double((long long)(s_red[2][0] - 1));
+          const double ys = __longlong_as_double((long long)s_red[3][0]);
+          const double e = sqrt(es) * (1.0 + 1e-12) + 1e-15 * sqrt(ys) + 1e-300;
+          atomicMax(tile_e + t, (unsigned long long)__double_as_longlong(
+                                    e == e ? e : __longlong_as_double(0x7ff8000000000000ll)));
+          if (rad_bits) {
+            const double rr = sqrt(__longlong_as_double((long long)s_red[4][0]));
+            atomicMax(rad_bits + t, (unsigned long long)__double_as_longlong(
+                                        rr == rr ? rr : __longlong_as_double(0x7ff8000000000000ll)));
+          }
         }
       }
+      __syncthreads();
+      sub = 0;
+      t += gridDim.x;
     }
   }
 }
@@ -1198,11 +1388,33 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   if (rad) BM_CHECK_CUDA(cudaMemsetAsync(rad, 0, n_tiles * 8, stream));
   BM_TRY(scratch_alloc(tp->s_lim, (size_t)n_tiles * 8, stream));
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_lim.ptr, 0, n_tiles * 8, stream));
-  quantize_kernel<<<grid_cap(P, 8, 32), 256, 0, stream>>>(
-      Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
-      reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
-      cen, reinterpret_cast<unsigned long long*>(rad), tp->s_lim.as<uint32_t>());
-  BM_CHECK_LAUNCH();
+  {
+    const int64_t stage = (int64_t)kQRows * d * 8;
+    const int n_stages = (int)std::min<int64_t>(kQMaxStages, (kQSmem - 16 * d) / stage);
+    auto args = [&](auto kern, unsigned grid, size_t smem) {
+      kern<<<grid, 256, smem, stream>>>(
+          Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
+          reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P),
+          tp->s_te.as<unsigned long long>(), cen, reinterpret_cast<unsigned long long*>(rad),
+          tp->s_lim.as<uint32_t>(), n_stages);
+    };
+    if (n_stages >= 2) {
+      static bool attr = false;
+      if (!attr) {
+        BM_CHECK_CUDA(cudaFuncSetAttribute(quantize_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem));
+        attr = true;
+      }
+      const size_t smem = (size_t)n_stages * stage + 16 * d;  // ring + two centres
+      const int per_sm = std::max<int>(1, std::min<int>(3, (int)((220 * 1024) / smem)));
+      args(quantize_kernel<true>,
+           (unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * per_sm), smem);
+    } else {
+      args(quantize_kernel<false>, (unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * 8),
+           0);
+    }
+    BM_CHECK_LAUNCH();
+  }
   BM_TRY(make_qmap(&tp->qmap, tp->s_pl.ptr, P, kpad));
 
   const double gamma = ((double)d + 16.0) * 1.5 * 1.1102230246251565e-16;

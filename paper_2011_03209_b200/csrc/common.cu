@@ -119,19 +119,30 @@ struct BigBuf {
   size_t bytes;
   int dev;
   bool busy;
+  cudaEvent_t ev;  // recorded on the holder's stream at release
+  bool pending;    // ev recorded and not yet waited on by a host free
 };
 std::mutex g_big_mu;
 std::vector<BigBuf> g_big;
+
+void big_free_locked(BigBuf& b) {  // g_big_mu held; b idle
+  if (b.pending) cudaEventSynchronize(b.ev);
+  b.pending = false;
+  cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
 }  // namespace
 
-int big_acquire(size_t bytes, void** out, int* slot) {
+int big_acquire(size_t bytes, cudaStream_t stream, void** out, int* slot) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_big_mu);
   int best = -1;
   for (int i = 0; i < (int)g_big.size(); ++i) {
     const BigBuf& b = g_big[i];
-    if (!b.busy && b.dev == dev && b.bytes >= bytes && (best < 0 || b.bytes < g_big[best].bytes))
+    if (!b.busy && b.p && b.dev == dev && b.bytes >= bytes &&
+        (best < 0 || b.bytes < g_big[best].bytes))
       best = i;
   }
   if (best < 0) {
@@ -140,11 +151,7 @@ int big_acquire(size_t bytes, void** out, int* slot) {
     if (e != cudaSuccess) {  // give back the idle cached buffers and retry once
       cudaGetLastError();
       for (auto& b : g_big)
-        if (!b.busy && b.dev == dev && b.p) {
-          cudaFree(b.p);
-          b.p = nullptr;
-          b.bytes = 0;
-        }
+        if (!b.busy && b.dev == dev && b.p) big_free_locked(b);
       e = cudaMalloc(&p, bytes);
     }
     if (e != cudaSuccess) {
@@ -152,8 +159,26 @@ int big_acquire(size_t bytes, void** out, int* slot) {
       set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
       return BM_ERR_NOMEM;
     }
-    g_big.push_back({p, bytes, dev, false});
-    best = (int)g_big.size() - 1;
+    for (int i = 0; i < (int)g_big.size() && best < 0; ++i)
+      if (!g_big[i].p && g_big[i].dev == dev) best = i;  // reuse an emptied entry
+    if (best < 0) {
+      BigBuf nb{};
+      nb.dev = dev;
+      if (cudaEventCreateWithFlags(&nb.ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
+        set_error("cudaEventCreate failed");
+        return BM_ERR_INTERNAL;
+      }
+      g_big.push_back(nb);
+      best = (int)g_big.size() - 1;
+    }
+    g_big[best].p = p;
+    g_big[best].bytes = bytes;
+    g_big[best].pending = false;
+  } else if (g_big[best].pending) {
+    // the previous holder's work on the buffer precedes this stream's use
+    cudaStreamWaitEvent(stream, g_big[best].ev, 0);
   }
   g_big[best].busy = true;
   *out = g_big[best].p;
@@ -161,9 +186,18 @@ int big_acquire(size_t bytes, void** out, int* slot) {
   return BM_OK;
 }
 
-void big_release(int slot) {
+void big_release(int slot, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_big_mu);
-  if (slot >= 0 && slot < (int)g_big.size()) g_big[slot].busy = false;
+  if (slot < 0 || slot >= (int)g_big.size()) return;
+  BigBuf& b = g_big[slot];
+  if (cudaEventRecord(b.ev, stream) == cudaSuccess) {
+    b.pending = true;
+  } else {  // cannot order the next use: drain the stream instead
+    cudaGetLastError();
+    cudaStreamSynchronize(stream);
+    b.pending = false;
+  }
+  b.busy = false;
 }
 
 void big_trim() {
@@ -171,11 +205,7 @@ void big_trim() {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_big_mu);
   for (auto& b : g_big)
-    if (!b.busy && b.dev == dev && b.p) {
-      cudaFree(b.p);
-      b.p = nullptr;
-      b.bytes = 0;
-    }
+    if (!b.busy && b.dev == dev && b.p) big_free_locked(b);
 }
 
 void release_pool() {

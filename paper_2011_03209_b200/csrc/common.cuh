@@ -87,30 +87,27 @@ void trace_mark(const char* name, cudaStream_t s);
 void trace_dump();
 
 // A large buffer kept across calls (cudaMalloc'd once per size class, reused
-// by later calls; bm_release_scratch frees the idle ones). The holder must not
-// release it before the stream's work on it has completed.
-int big_acquire(size_t bytes, void** out, int* slot);
-void big_release(int slot);
+// by later calls; bm_release_scratch frees the idle ones). Release records an
+// event on the holder's stream and the next holder's stream waits on it, so
+// reuse is stream-ordered without host synchronisation.
+int big_acquire(size_t bytes, cudaStream_t stream, void** out, int* slot);
+void big_release(int slot, cudaStream_t stream);
 struct BigScratch {
   void* ptr = nullptr;
   int slot = -1;
-  cudaStream_t stream = nullptr;  // work on the buffer is drained before release
+  cudaStream_t stream = nullptr;
   BigScratch() = default;
   BigScratch(const BigScratch&) = delete;
   BigScratch& operator=(const BigScratch&) = delete;
-  ~BigScratch() {
-    if (slot >= 0 && stream) cudaStreamSynchronize(stream);
-    big_release(slot);
-  }
+  ~BigScratch() { big_release(slot, stream); }
   template <typename T>
   T* as() const { return reinterpret_cast<T*>(ptr); }
 };
 inline int big_scratch(BigScratch& b, size_t bytes, cudaStream_t stream) {
-  if (b.slot >= 0 && b.stream) cudaStreamSynchronize(b.stream);
-  big_release(b.slot);
+  big_release(b.slot, b.stream);
   b.slot = -1;
   b.stream = stream;
-  return big_acquire(bytes, &b.ptr, &b.slot);
+  return big_acquire(bytes, stream, &b.ptr, &b.slot);
 }
 
 // Free device memory including what the stream-ordered pool retains unused.

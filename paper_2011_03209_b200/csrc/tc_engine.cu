@@ -1481,7 +1481,8 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   const int64_t P = tp->P, d = tp->d;
   const int nkc = tp->nkc;
   if (n_units == 0) return BM_OK;
-  Scratch s_q, s_cnt, s_tt;
+  Scratch s_cnt, s_tt;
+  BigScratch s_q;  // cached across calls: mapping ~100 MB per call costs ~1 ms
   int32_t* cnt_run = cnt;
   if (accumulate || !cnt) {  // window counts go to a private buffer first
     if (!tp->s_cntw.ptr) BM_TRY(scratch_alloc(tp->s_cntw, (size_t)P * 4, stream));
@@ -1508,7 +1509,11 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   trace_mark("tc:thr allocated", stream);
   unsigned long long h_cnt[2] = {0, 0};
   for (int attempt = 0; attempt < 3; ++attempt) {
-    BM_TRY(scratch_alloc(s_q, qcap * sizeof(int4), stream));
+    {
+      size_t qb = (size_t)16 << 20;  // power-of-two size classes
+      while (qb < qcap * sizeof(int4)) qb <<= 1;
+      BM_TRY(big_scratch(s_q, qb, stream));
+    }
     trace_mark("tc:queue allocated", stream);
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));

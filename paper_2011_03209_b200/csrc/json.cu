@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -18,6 +19,36 @@
 
 namespace bm {
 namespace {
+
+// two decimal digits per step
+constexpr char kDigits2[] =
+    "00010203040506070809101112131415161718192021222324252627282930313233343536373839"
+    "40414243444546474849505152535455565758596061626364656667686970717273747576777879"
+    "8081828384858687888990919293949596979899";
+
+// decimal text of v at p (no bounds check; <= 20 bytes), returns the end
+inline char* fmt_int(char* p, int64_t v) {
+  uint64_t u = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
+  if (v < 0) *p++ = '-';
+  char t[20];
+  int n = 20;
+  while (u >= 100) {
+    const unsigned r = (unsigned)(u % 100);
+    u /= 100;
+    n -= 2;
+    t[n] = kDigits2[2 * r];
+    t[n + 1] = kDigits2[2 * r + 1];
+  }
+  if (u >= 10) {
+    n -= 2;
+    t[n] = kDigits2[2 * u];
+    t[n + 1] = kDigits2[2 * u + 1];
+  } else {
+    t[--n] = (char)('0' + u);
+  }
+  memcpy(p, t + n, 20 - n);
+  return p + 20 - n;
+}
 
 struct Out {
   char* buf;
@@ -29,14 +60,23 @@ struct Out {
   void put(const char* s) { put(s, (int64_t)strlen(s)); }
   void put_int(int64_t v) {
     char t[24];
-    int n = 0;
-    uint64_t u = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
-    do {
-      t[23 - n++] = (char)('0' + u % 10);
-      u /= 10;
-    } while (u);
-    if (v < 0) t[23 - n++] = '-';
-    put(t + 24 - n, n);
+    put(t, fmt_int(t, v) - t);
+  }
+  // comma-separated ints; unchecked fast path when the worst case fits
+  void put_ints(const int64_t* a, int64_t n) {
+    if (buf && len + 21 * n <= cap) {
+      char* p = buf + len;
+      for (int64_t i = 0; i < n; ++i) {
+        if (i) *p++ = ',';
+        p = fmt_int(p, a[i]);
+      }
+      len = p - buf;
+      return;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      if (i) put(",", 1);
+      put_int(a[i]);
+    }
   }
   // "%.9g" exactly as Python's '%.9g' % v (both correctly rounded; same
   // exponent rules), "-0" -> "0"
@@ -89,10 +129,7 @@ bool write_nodes(Out& o, int64_t v0, int64_t v1, const int64_t* h_node_rows,
     o.put("],\"id\":");
     o.put_int(v);
     o.put(",\"rows\":[");
-    for (int64_t e = h_node_off[v]; e < h_node_off[v + 1]; ++e) {
-      if (e > h_node_off[v]) o.put(",", 1);
-      o.put_int(h_node_rows[e]);
-    }
+    o.put_ints(h_node_rows + h_node_off[v], h_node_off[v + 1] - h_node_off[v]);
     o.put("],\"size\":");
     o.put_int(h_node_off[v + 1] - h_node_off[v]);
     o.put(",\"stats\":{");
@@ -124,53 +161,115 @@ extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
   BM_REQUIRE(d == 0 || (h_stats && h_stat_order && h_names && h_name_off), "null stats table");
   BM_REQUIRE(m == 0 || h_fmean, "null filter means");
   // node ranges of balanced byte volume are written by host threads into
-  // private buffers, then concatenated in order
-  const int64_t total = n_nodes ? h_node_off[n_nodes] : 0;
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, total / 65536));
-  std::vector<int64_t> cut(nt + 1, n_nodes);
-  cut[0] = 0;
-  for (int t = 1, v = 0; t < nt; ++t) {
-    while (v < n_nodes && h_node_off[v] < total * t / nt) ++v;
-    cut[t] = v;
-  }
-  std::vector<std::vector<char>> parts(nt);
-  std::vector<int> ok(nt, 1);
-  auto work = [&](int t) {
-    const int64_t v0 = cut[t], v1 = std::max(cut[t], cut[t + 1]);
-    const int64_t est = (h_node_off[v1] - h_node_off[v0]) * 8 + (v1 - v0) * (d + m + 8) * 18 + 64;
-    parts[t].resize(est);
-    for (;;) {
-      Out o{parts[t].data(), (int64_t)parts[t].size()};
-      ok[t] = write_nodes(o, v0, v1, h_node_rows, h_node_off, h_elem, h_stats, d, h_stat_order,
-                          h_names, h_name_off, h_fmean, m, h_comp, h_comp_off);
-      if (o.len <= (int64_t)parts[t].size()) {
-        parts[t].resize(o.len);
-        return;
-      }
-      parts[t].resize(o.len);  // estimate too small: rewrite at the exact size
+  // private buffers (kept across calls: no page faults on reuse), then copied
+  // in order into out by the same threads. A sizing call (out == NULL) keeps
+  // its formatted parts for this thread, and the next call with the same
+  // arguments only copies them.
+  struct Key {
+    const void* p[10];
+    int64_t n, d;
+    int32_t m;
+    bool operator==(const Key& o) const {
+      return n == o.n && d == o.d && m == o.m && memcmp(p, o.p, sizeof p) == 0;
     }
   };
-  if (nt == 1) {
-    work(0);
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) th.emplace_back(work, t);
-    for (auto& x : th) x.join();
-  }
-  for (int t = 0; t < nt; ++t)
-    if (!ok[t]) {
-      set_error("non-finite value in graph JSON");
-      return BM_ERR_DATA;
+  const Key key{{h_node_rows, h_node_off, h_elem, h_stats, h_stat_order, h_names, h_name_off,
+                 h_fmean, h_comp, h_comp_off},
+                n_nodes, d, m};
+  struct Cache {
+    bool valid = false;
+    Key key{};
+    std::vector<std::vector<char>> parts;
+    std::vector<int64_t> len;
+  };
+  thread_local Cache cache;
+  static std::mutex pool_mu;
+  static std::vector<std::vector<char>> pool;  // idle part buffers
+  auto give_back = [&](std::vector<std::vector<char>>& parts) {
+    std::lock_guard<std::mutex> lk(pool_mu);
+    for (auto& p : parts)
+      if (pool.size() < 64) pool.emplace_back(std::move(p));
+    parts.clear();
+  };
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  auto run = [&](int nt, auto fn) {
+    if (nt == 1) {
+      fn(0);
+      return;
     }
-  Out o{out, out ? cap : 0};
-  o.put("[", 1);
-  for (int t = 0; t < nt; ++t) o.put(parts[t].data(), (int64_t)parts[t].size());
-  o.put("]", 1);
-  *h_len = o.len;
-  if (out && o.len > cap) {
-    set_error("output buffer too small (%lld < %lld)", (long long)cap, (long long)o.len);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(fn, t);
+    for (auto& x : th) x.join();
+  };
+  std::vector<std::vector<char>> parts;
+  std::vector<int64_t> len;
+  if (out && cache.valid && cache.key == key) {
+    parts.swap(cache.parts);
+    len.swap(cache.len);
+    cache.valid = false;
+  } else {
+    if (cache.valid) {
+      give_back(cache.parts);
+      cache.valid = false;
+    }
+    const int64_t total = n_nodes ? h_node_off[n_nodes] : 0;
+    const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, total / 32768));
+    std::vector<int64_t> cut(nt + 1, n_nodes);
+    cut[0] = 0;
+    for (int t = 1, v = 0; t < nt; ++t) {
+      while (v < n_nodes && h_node_off[v] < total * t / nt) ++v;
+      cut[t] = v;
+    }
+    parts.resize(nt);
+    {
+      std::lock_guard<std::mutex> lk(pool_mu);
+      for (int t = 0; t < nt && !pool.empty(); ++t) {
+        parts[t].swap(pool.back());
+        pool.pop_back();
+      }
+    }
+    len.assign(nt, 0);
+    std::vector<int> ok(nt, 1);
+    run(nt, [&](int t) {
+      const int64_t v0 = cut[t], v1 = std::max(cut[t], cut[t + 1]);
+      const int64_t est =
+          (h_node_off[v1] - h_node_off[v0]) * 8 + (v1 - v0) * (d + m + 8) * 18 + 64;
+      if ((int64_t)parts[t].size() < est) parts[t].resize(est);
+      for (;;) {
+        Out o{parts[t].data(), (int64_t)parts[t].size()};
+        ok[t] = write_nodes(o, v0, v1, h_node_rows, h_node_off, h_elem, h_stats, d,
+                            h_stat_order, h_names, h_name_off, h_fmean, m, h_comp, h_comp_off);
+        len[t] = o.len;
+        if (o.len <= (int64_t)parts[t].size()) return;
+        parts[t].resize(o.len);  // estimate too small: rewrite at the exact size
+      }
+    });
+    for (int t = 0; t < nt; ++t)
+      if (!ok[t]) {
+        give_back(parts);
+        set_error("non-finite value in graph JSON");
+        return BM_ERR_DATA;
+      }
+  }
+  const int nt = (int)parts.size();
+  std::vector<int64_t> at(nt + 1, 1);  // "[" first
+  for (int t = 0; t < nt; ++t) at[t + 1] = at[t] + len[t];
+  *h_len = at[nt] + 1;  // "]"
+  if (!out) {  // sizing call: keep the parts for the writing call
+    cache.parts.swap(parts);
+    cache.len.swap(len);
+    cache.key = key;
+    cache.valid = true;
+    return BM_OK;
+  }
+  if (*h_len > cap) {
+    give_back(parts);
+    set_error("output buffer too small (%lld < %lld)", (long long)cap, (long long)*h_len);
     return BM_ERR_DATA;
   }
+  out[0] = '[';
+  run(nt, [&](int t) { memcpy(out + at[t], parts[t].data(), len[t]); });
+  out[at[nt]] = ']';
+  give_back(parts);
   return BM_OK;
 }

@@ -236,28 +236,69 @@ __global__ void sparse_edges_kernel(const uint64_t* __restrict__ keys, int64_t n
 }
 
 // ---- node payload ------------------------------------------------------------
-// stats: numpy X[rows].mean(axis=0) = sequential row sum per column / size
-__global__ void node_stats_kernel(const double* __restrict__ X, int64_t d,
-                                  const int64_t* __restrict__ node_rows,
-                                  const int64_t* __restrict__ node_off, int64_t n_nodes,
-                                  double* __restrict__ stats) {
+// stats: numpy X[rows].mean(axis=0) = sequential row sum per column / size.
+// The row sum is an inherently serial fp64 chain per column, so the time is
+// set by how many row loads are in flight per chain: one warp per (node, 32
+// columns) streams its rows through a shared-memory ring of kNsStages chunks
+// of 32 rows with cp.async (each lane copies, and then adds, its own column;
+// 192 rows in flight per warp), row ids prefetched a chunk ahead.
+constexpr int kNsStages = 6;  // 48 KB of static shared memory
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool pred) {
+  const unsigned sz = pred ? 8u : 0u;  // src-size 0: zero-fill, no read
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(sz)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+node_stats_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ node_rows,
+                  const int64_t* __restrict__ node_off, int64_t n_nodes,
+                  double* __restrict__ stats) {
+  __shared__ __align__(16) double ring[kNsStages][32][32];
   const int64_t v = blockIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= n_nodes || c >= d) return;
+  const int lane = threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const bool col = c < d;
   const int64_t a = node_off[v], b = node_off[v + 1];
-  // numpy axis-0 mean: the rows are added in order (an inherently serial
-  // fp64 chain); 32 row loads are in flight ahead of the dependent additions
+  const int64_t n_chunks = (b - a + 31) / 32;
+  const double* Xc = X + (col ? c : 0);
+  int64_t idx = a + lane < b ? node_rows[a + lane] : 0;  // row ids of the next chunk to issue
+  int64_t q = 0;                                          // next chunk to issue
+  auto issue = [&]() {
+    if (q < n_chunks) {
+      const int64_t base = a + q * 32;
+      const int64_t nxt = base + 32 + lane;
+      const int64_t idx_next = nxt < b ? node_rows[nxt] : 0;
+      double(*st)[32] = ring[q % kNsStages];
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const int64_t r = __shfl_sync(0xffffffffu, idx, j);
+        cp_async8(&st[j][lane], Xc + r * d, col && base + j < b);
+      }
+      idx = idx_next;
+    }
+    ++q;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll 1
+  for (int s0 = 0; s0 < kNsStages - 1; ++s0) issue();
   double s = 0.0;
-  int64_t i = a;
-  for (; i + 32 <= b; i += 32) {
-    double x[32];
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    issue();
+    asm volatile("cp.async.wait_group %0;" ::"n"(kNsStages - 1) : "memory");
+    const double(*st)[32] = ring[k % kNsStages];
+    const int nv = (int)min((int64_t)32, b - (a + k * 32));
+    if (nv == 32) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = X[node_rows[i + j] * d + c];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) s = __dadd_rn(s, x[j]);
+      for (int j = 0; j < 32; ++j) s = __dadd_rn(s, st[j][lane]);
+    } else {
+      for (int j = 0; j < nv; ++j) s = __dadd_rn(s, st[j][lane]);
+    }
   }
-  for (; i < b; ++i) s = __dadd_rn(s, X[node_rows[i] * d + c]);
-  stats[v * d + c] = __ddiv_rn(s, (double)(b - a));
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (col) stats[v * d + c] = __ddiv_rn(s, (double)(b - a));
 }
 
 // numpy 1-D mean of the filter values of every node, in two parallel steps:
@@ -487,8 +528,8 @@ extern "C" int bm_node_stats(const double* d_X, int64_t d, const double* d_f, in
   BM_REQUIRE(n_nodes <= 65535, "node_stats: at most 65535 nodes per call");
   if (d_stats) {
     BM_REQUIRE(d_X, "null points");
-    dim3 grid((unsigned)ceil_div(d, 128), (unsigned)n_nodes);
-    node_stats_kernel<<<grid, 128, 0, s>>>(d_X, d, d_node_rows, d_node_offsets, n_nodes, d_stats);
+    dim3 grid((unsigned)ceil_div(d, 32), (unsigned)n_nodes);
+    node_stats_kernel<<<grid, 32, 0, s>>>(d_X, d, d_node_rows, d_node_offsets, n_nodes, d_stats);
     BM_CHECK_LAUNCH();
   }
   if (d_fmean) {

@@ -1218,28 +1218,44 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
 // the row counts): one warp per (tile, 32-column word), 4 row quarters
 // transposed in registers (lane j then holds column j), popc, one atomic per
 // column. Runs before the recheck, which counts the bits it adds itself.
-__global__ void __launch_bounds__(128)
+// One warp per kept off-diagonal tile: the 128 x 4 words arrive as four
+// 16-byte loads per lane (row 32 rb + lane), issued before any transpose; the
+// next tile's flags are fetched one tile ahead.
+__global__ void __launch_bounds__(256)
 colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ nonempty,
                 const TileRef* __restrict__ tiles, int64_t slot0, int64_t n_tiles,
                 ElemTables et, int32_t* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t s = blockIdx.x; s < n_tiles; s += gridDim.x) {
-    if (!nonempty[s]) continue;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t s = w0;
+  int ne = s < n_tiles ? nonempty[s] : 0;
+  for (; s < n_tiles; s += nw) {
+    const int ne_cur = ne;
+    ne = s + nw < n_tiles ? nonempty[s + nw] : 0;
+    if (!ne_cur) continue;
     const TileRef tr = tiles[slot0 + s];
     if (tr.I == tr.J) continue;
-    const uint32_t* b = adj + s * kTileWords;
-    int acc = 0;
+    const uint4* b = reinterpret_cast<const uint4*>(adj + s * kTileWords);
+    uint4 r[4];
 #pragma unroll
-    for (int rb = 0; rb < 4; ++rb) {
-      uint32_t x = b[(rb * 32 + lane) * 4 + w];
-      x = bit_transpose_step(x, 16, 0x0000FFFFu, lane);
-      x = bit_transpose_step(x, 8, 0x00FF00FFu, lane);
-      x = bit_transpose_step(x, 4, 0x0F0F0F0Fu, lane);
-      x = bit_transpose_step(x, 2, 0x33333333u, lane);
-      x = bit_transpose_step(x, 1, 0x55555555u, lane);
-      acc += __popc(x);
+    for (int rb = 0; rb < 4; ++rb) r[rb] = b[rb * 32 + lane];
+    const int64_t base = et.pbase[tr.k] + tr.J * kTile + lane;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      int acc = 0;
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) {
+        uint32_t x = w == 0 ? r[rb].x : w == 1 ? r[rb].y : w == 2 ? r[rb].z : r[rb].w;
+        x = bit_transpose_step(x, 16, 0x0000FFFFu, lane);
+        x = bit_transpose_step(x, 8, 0x00FF00FFu, lane);
+        x = bit_transpose_step(x, 4, 0x0F0F0F0Fu, lane);
+        x = bit_transpose_step(x, 2, 0x33333333u, lane);
+        x = bit_transpose_step(x, 1, 0x55555555u, lane);
+        acc += __popc(x);
+      }
+      if (acc) atomicAdd(cnt + base + w * 32, acc);
     }
-    if (acc) atomicAdd(cnt + et.pbase[tr.k] + tr.J * kTile + w * 32 + lane, acc);
   }
 }
 
@@ -1589,8 +1605,8 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
       return BM_ERR_INTERNAL;
     }
   }
-  colcount_kernel<<<grid_cap(n_tiles, 1, 16), 128, 0, stream>>>(adj, nonempty, tiles, slot0,
-                                                                n_tiles, et, cnt_run);
+  colcount_kernel<<<grid_cap(n_tiles, 8, 8), 256, 0, stream>>>(adj, nonempty, tiles, slot0,
+                                                               n_tiles, et, cnt_run);
   BM_CHECK_LAUNCH();
   {
     // the queue length stays on the device: the recheck grid covers the

@@ -390,7 +390,11 @@ tile_project_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et, int
   const int k = (int)lo;
   const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
   const float* sfk = sf + (int64_t)k * kGroupSeeds * d;
-  const int t = threadIdx.x, ty = t >> 3, tx = t & 7;  // points 4ty.., seeds 8tx..
+  // points 4ty.., seeds 8tx..; a warp covers 8 point groups x 4 seed groups,
+  // so its shared-memory operand loads touch 8 + 4 distinct 16-byte vectors
+  // (no bank conflicts; 3 wavefronts per k step)
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  const int ty = (lane & 7) + 8 * (wp & 3), tx = (lane >> 3) + 4 * (wp >> 2);
   float acc[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)

@@ -112,7 +112,7 @@ gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
 // tiles compact, so tile pairs of far-apart groups can be pruned.
 // ---------------------------------------------------------------------------
 constexpr int kGroupSeeds = 64;
-static_assert(kGroupSeeds == 64, "group_assign_kernel gives each lane two seeds (lane, lane + 32)");
+static_assert(kGroupSeeds == 64, "seed_order / tile_project / prune kernels are written for 64 seeds");
 constexpr int kGroupDims = 32;
 constexpr int kGroupMinRows = 3 * kTile;  // smaller elements keep their order
 
@@ -187,62 +187,52 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
   }
 }
 
+// One thread per entry: its first kGroupDims coordinates in registers
+// (fp32), the 64 seeds broadcast from shared memory, 4 dims per 16-byte
+// load; nearest seed (smallest index on ties) -> key (element, seed rank).
 __global__ void __launch_bounds__(128)
 group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                     const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
                     const int32_t* __restrict__ seed_rank, uint64_t* __restrict__ keys,
                     int64_t* __restrict__ vals) {
-  __shared__ float sd[kGroupDims][kGroupSeeds];  // seed coordinates, [dim][seed]
+  __shared__ __align__(16) float sd[kGroupSeeds][kGroupDims];  // seed coordinates
   const GroupItem it = items[blockIdx.x];
   const int64_t ek = offs[it.k], nk = offs[it.k + 1] - ek;
   const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
   const int D = d < kGroupDims ? (int)d : kGroupDims;
   for (int i = threadIdx.x; i < kGroupDims * kGroupSeeds; i += blockDim.x) {
-    const int dim = i / kGroupSeeds, j = i % kGroupSeeds;
-    float v = 3.0e38f;  // unused seeds are far away
+    const int j = i / kGroupDims, dim = i % kGroupDims;
+    float v = 0.0f;  // dims >= D are 0 on both sides
     if (j < S && dim < D) v = (float)X[rows[ek + (j * nk) / S] * d + dim];
-    else if (j < S) v = 0.0f;
-    sd[dim][j] = v;
+    sd[j][dim] = v;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  static_assert(kGroupDims <= 32, "one dim per lane");
-  const int nw = blockDim.x >> 5;
-  int e = it.e0 + (threadIdx.x >> 5);
-  // the next entry's coordinates are loaded while the current one is scored
-  float xn = (e < it.e1 && lane < D) ? (float)X[rows[e] * d + lane] : 0.0f;
-  for (; e < it.e1; e += nw) {
-    const float x0 = xn;
-    const int en = e + nw;
-    xn = (en < it.e1 && lane < D) ? (float)X[rows[en] * d + lane] : 0.0f;
-    float d0 = 0.0f, d1 = 0.0f;  // seeds lane, lane + 32 (dims >= D are 0 on both sides)
+  for (int e = it.e0 + threadIdx.x; e < it.e1; e += blockDim.x) {
+    const double* xr = X + rows[e] * d;
+    float x[kGroupDims];
 #pragma unroll
-    for (int dim = 0; dim < kGroupDims; ++dim) {
-      const float xv = __shfl_sync(0xffffffffu, x0, dim);
-      const float a = xv - sd[dim][lane], b = xv - sd[dim][lane + 32];
-      d0 = fmaf(a, a, d0);
-      d1 = fmaf(b, b, d1);
-    }
-    if (lane >= S) d0 = 3.0e38f;
-    if (lane + 32 >= S) d1 = 3.0e38f;
-    float best = d0;
-    int bi = lane;
-    if (d1 < best) {
-      best = d1;
-      bi = lane + 32;
-    }
-    for (int o = 16; o; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob < best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
+    for (int c = 0; c < kGroupDims; ++c) x[c] = c < D ? (float)xr[c] : 0.0f;
+    float best = 3.0e38f;
+    int bi = 0;
+    for (int j = 0; j < S; ++j) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kGroupDims; c += 4) {
+        const float4 sv = *reinterpret_cast<const float4*>(&sd[j][c]);
+        const float a0 = x[c] - sv.x, a1 = x[c + 1] - sv.y, a2 = x[c + 2] - sv.z,
+                    a3 = x[c + 3] - sv.w;
+        acc = fmaf(a0, a0, acc);
+        acc = fmaf(a1, a1, acc);
+        acc = fmaf(a2, a2, acc);
+        acc = fmaf(a3, a3, acc);
+      }
+      if (acc < best) {
+        best = acc;
+        bi = j;
       }
     }
-    if (lane == 0) {
-      keys[e] = ((uint64_t)it.k << 7) | (uint64_t)seed_rank[(int64_t)it.k * kGroupSeeds + bi];
-      vals[e] = e;
-    }
+    keys[e] = ((uint64_t)it.k << 7) | (uint64_t)seed_rank[(int64_t)it.k * kGroupSeeds + bi];
+    vals[e] = e;
   }
 }
 

@@ -51,7 +51,10 @@ extern "C" {
 /* Distance engines for bm_cluster_elements (flags) */
 #define BM_ENGINE_AUTO 0  /* tensor-core candidates + exact recheck where supported */
 #define BM_ENGINE_EXACT 1 /* every pair evaluated in exact fp64 order on CUDA cores   */
-#define BM_ENGINE_TC 2    /* force the tcgen05 candidate engine                        */
+#define BM_ENGINE_TC 2    /* force the tcgen05 candidate engine (32 <= d <= 256:
+                             full-K operand tiles live in shared memory; outside
+                             that range BM_ENGINE_TC is BM_ERR_DATA and AUTO
+                             uses the exact engine) */
 
 int bm_abi_version(void);
 const char* bm_last_error(void);

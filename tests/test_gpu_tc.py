@@ -26,7 +26,7 @@ def labels(X, members, eps, min_pts, orders, engine):
     return lab.cpu().numpy(), ncl, st
 
 
-@pytest.mark.parametrize("d", [32, 48, 64, 100, 128, 129, 200, 256])
+@pytest.mark.parametrize("d", [32, 48, 64, 100, 128, 129, 200, 255, 256])
 @pytest.mark.parametrize("q", [0.02, 0.15])
 def test_tc_equals_exact(d, q):
     rng = np.random.default_rng(d)
@@ -74,6 +74,38 @@ def test_tc_large_offsets_and_nan():
     b, nb, _ = labels(X, [rows], eps, 3, [0], 2)
     assert np.array_equal(a, b) and np.array_equal(na, nb)
     assert a[17] == -1  # NaN point is in no neighbourhood (sqrt(NaN) <= eps is False)
+
+
+@pytest.mark.parametrize("d", [16, 257])
+def test_tc_dimension_range(d):
+    """The tensor-core engine covers 32 <= d <= 256 (full-K B tiles in shared
+    memory); asking for it outside raises DataError, the automatic engine
+    takes the exact fp64 engine there."""
+    from paper_2011_03209_b200.errors import DataError
+
+    X = O.gmm(400, d, 3, 2.0, d)
+    eps = O.dist_quantile(X, 0.1)
+    rows = np.arange(400)
+    with pytest.raises(DataError, match="tensor-core engine does not support"):
+        labels(X, [rows], eps, 3, [0], 2)
+    a, na, _ = labels(X, [rows], eps, 3, [0], 0)
+    b, nb, _ = labels(X, [rows], eps, 3, [0], 1)
+    assert np.array_equal(a, b) and np.array_equal(na, nb)
+
+
+def test_tc_infinite_coordinates():
+    """Rows with +-inf take the quantiser's clamping path (redone per row);
+    they are in no neighbourhood, like NaN rows."""
+    X = O.gmm(900, 96, 3, 2.0, 5)
+    eps = O.dist_quantile(X, 0.1)
+    X[3, 7] = np.inf
+    X[400, 0] = -np.inf
+    X[401, 95] = 1e300
+    rows = np.arange(900)
+    a, na, _ = labels(X, [rows], eps, 3, [0], 1)
+    b, nb, _ = labels(X, [rows], eps, 3, [0], 2)
+    assert np.array_equal(a, b) and np.array_equal(na, nb)
+    assert a[3] == -1 and a[400] == -1
 
 
 @pytest.mark.parametrize("qcap", ["40", "3"])

@@ -781,22 +781,22 @@ __global__ void elem_scale_kernel(int64_t n_el, const unsigned long long* __rest
   scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
 }
 
-// one block per tile, one warp per padded row: limbs into the three planes (4
-// columns per lane, packed 32-bit stores), N = sum q^2 (exact),
-// e = |x - c - s q| (fp64) -> tile max (bit pattern, one atomicMax per tile);
-// with cen != null also the row's distance to its tile centre -> tile radius
-// (raw max, NaN-propagating).
-// BULK: the block's rows stream through a shared-memory ring of kQRows-row
-// stages filled by cp.async.bulk (a tile is 128 contiguous rows of Xg), so
-// tens of KB per SM are in flight instead of one register load per lane.
-constexpr int kQWarps = 8;  // blockDim.x == 256
-constexpr int kQRows = kQWarps;  // rows per ring stage (one per warp)
+// One block per tile (grid-stride), one HALF-warp per padded row: limbs into
+// the three planes (4 columns per lane per pass, packed 32-bit stores),
+// N = sum q^2 (exact), e = |x - c - s q| (fp64) -> tile max (bit pattern, one
+// atomicMax per tile); with cen != null also the row's distance to its tile
+// centre -> tile radius (raw max, NaN-propagating). The block's rows stream
+// through a shared-memory ring of kQRows-row stages filled by cp.async.bulk
+// (a tile is 128 contiguous rows of Xg); the element and tile centres are
+// staged once per tile. Two rows per warp halve the per-row reduction and
+// bookkeeping instructions (the kernel is issue-bound, not HBM-bound).
+constexpr int kQWarps = 8;            // blockDim.x == 256
+constexpr int kQRows = 2 * kQWarps;   // rows per ring stage (one per half-warp)
 constexpr int kQIters = kTile / kQRows;
 constexpr int kQMaxStages = 4;
-constexpr int kQSmem = 96 * 1024;  // ring budget
+constexpr int kQSmem = 96 * 1024;     // ring budget (d <= 256: 2 stages of 32 KB + centres)
 
-template <bool BULK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTables et, int64_t P,
                 const double* __restrict__ center, const double* __restrict__ scale,
                 int8_t* __restrict__ planes, int64_t* __restrict__ nq, int32_t* __restrict__ cq,
@@ -805,36 +805,39 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
                 int n_stages) {
   extern __shared__ __align__(128) double q_ring[];
   __shared__ __align__(8) uint64_t q_full[kQMaxStages];
-  __shared__ unsigned long long s_red[5][kQWarps];
+  __shared__ unsigned long long s_red[5][2 * kQWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane >> 4, hl = lane & 15, hrow = 2 * warp + half;
   const int64_t n_tiles = P / kTile;
   const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t n_it = my_tiles * kQIters;
   const uint32_t stage_bytes = (uint32_t)(kQRows * d * 8);
+  double* const s_c = q_ring + n_stages * kQRows * d;  // element centre, tile centre
   auto issue = [&](int64_t i, int sl) {  // iteration i into ring slot sl
     const int64_t row0 = (blockIdx.x + (i / kQIters) * gridDim.x) * kTile + (i % kQIters) * kQRows;
     uint64_t* bar = q_full + sl;
     mbar_expect_tx(bar, stage_bytes);
     bulk_load(q_ring + sl * kQRows * d, Xg + row0 * d, stage_bytes, bar);
   };
-  if (BULK) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < n_stages; ++i) mbar_init(q_full + i, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int i = 0; i < n_stages && i < n_it; ++i) issue(i, i);
-    }
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n_stages; ++i) mbar_init(q_full + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < n_stages && i < n_it; ++i) issue(i, i);
   }
+  __syncthreads();
   int k = 0;
   double sc = 1.0, inv = 1.0;
-  // per-warp maxima over its rows (lane 0): |M|^2, |L|^2 and the bit patterns
-  // of the squared error / |x - c|^2 / radius sums (square roots per tile)
+  // per-half-warp maxima over its rows (lane hl == 0): |M|^2, |L|^2 and the
+  // bit patterns of the squared error / |y|^2 / radius sums (roots per tile)
   unsigned long long w_m = 0, w_l = 0, w_e = 0, w_y = 0, w_r = 0;
   bool w_valid = false;
   int slot = 0;
   uint32_t phase = 0;
   int64_t t = blockIdx.x;
   int sub = 0;  // row group within the tile
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr double kQMax = (double)((1 << kQBits) - 1);
+  const bool vec = (d & 1) == 0;  // 16-byte aligned rows in the ring
   for (int64_t i = 0; i < n_it; ++i) {
     if (sub == 0) {
       int64_t a = 0, bb = et.n_el;
@@ -847,45 +850,33 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
       inv = 1.0 / sc;
       w_m = w_l = w_e = w_y = w_r = 0;
       w_valid = false;
-      if (BULK) {  // the element centre and the tile centre, once per tile
-        double* s_c = q_ring + n_stages * kQRows * d;
-        for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-          s_c[c] = center[(int64_t)k * d + c];
-          s_c[d + c] = cen ? cen[t * d + c] : 0.0;
-        }
-        __syncthreads();
+      for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+        s_c[c] = center[(int64_t)k * d + c];
+        s_c[d + c] = cen ? cen[t * d + c] : 0.0;
       }
+      __syncthreads();
     }
-    const int64_t p = t * kTile + sub * kQRows + warp;
-    const double* xr;
-    if (BULK) {
-      mbar_wait(q_full + slot, phase);
-      xr = q_ring + slot * kQRows * d + warp * d;
-    } else {
-      xr = Xg + p * d;
-    }
+    const int64_t p = t * kTile + sub * kQRows + hrow;
+    mbar_wait(q_full + slot, phase);
+    const double* xr = q_ring + slot * kQRows * d + hrow * d;
     const bool valid = (p - et.pbase[k]) < et.nrows[k];
-    const double* ck = BULK ? q_ring + n_stages * kQRows * d : center + (int64_t)k * d;
-    const double* ct = cen ? (BULK ? ck + d : cen + t * d) : nullptr;
-    long long nsum = 0;
+    const double* ck = s_c;
+    const double* ct = cen ? s_c + d : nullptr;
     uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
-    double esum = 0.0, ysum = 0.0, rsum = 0.0;
-    int8_t* const hrow = planes + p * kpad;
-    int8_t* const mrow = planes + P * kpad + p * kpad;
-    int8_t* const lrow = planes + 2 * P * kpad + p * kpad;
+    double esum = 0.0, ysum = 0.0, rsum = 0.0, nsd = 0.0;
+    int8_t* const hrow_p = planes + p * kpad;
+    int8_t* const mrow_p = planes + P * kpad + p * kpad;
+    int8_t* const lrow_p = planes + 2 * P * kpad + p * kpad;
     // Fast path (full 4-column groups of a valid row): rint and the integer
     // conversion by the 1.5 * 2^52 trick (exact rint, ties to even, for
     // |v| < 2^51), byte packing with PRMT, limb norms with DP4A, sum q^2 in
-    // fp64 (per lane <= 256 * 2^42 < 2^53: exact). A row with any
-    // |v| >= qmax (clamping, inf, NaN) is redone by the generic path.
-    constexpr double kMagic = 6755399441055744.0;
-    constexpr double kQMax = (double)((1 << kQBits) - 1);
+    // fp64 (per lane <= 16 * 2^42: exact). A row with any |v| >= qmax
+    // (clamping, inf, NaN) is redone by the generic path.
     bool bad = false;
-    double nsd = 0.0;
     if (valid) {
-      for (int64_t c4 = 4 * lane; c4 < kpad && c4 + 4 <= d; c4 += 128) {
+      for (int64_t c4 = 4 * hl; c4 < kpad && c4 + 4 <= d; c4 += 64) {
         double xv[4], cv[4], tv[4];
-        if (BULK && (d & 1) == 0) {  // shared memory, 16-byte aligned
+        if (vec) {
           const double2 u0 = *reinterpret_cast<const double2*>(xr + c4);
           const double2 u1 = *reinterpret_cast<const double2*>(xr + c4 + 2);
           xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
@@ -933,16 +924,16 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
             __byte_perm(q[2] >> (2 * kLimb), q[3] >> (2 * kLimb), 0x0040), 0x5410);
         msq = __dp4a(mw, mw, msq);
         lsq = __dp4a(lw, lw, lsq);
-        *reinterpret_cast<uint32_t*>(hrow + c4) = hw;
-        *reinterpret_cast<uint32_t*>(mrow + c4) = mw;
-        *reinterpret_cast<uint32_t*>(lrow + c4) = lw;
+        *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
+        *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
+        *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
       }
     }
-    nsum = (long long)nsd;
-    const bool redo = __any_sync(0xffffffffu, bad);
+    unsigned long long nsum = (unsigned long long)nsd;
+    const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
     if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
     // generic path: the tail columns (or the whole row when redo / padding)
-    for (int64_t c4 = 4 * lane; c4 < kpad; c4 += 128) {
+    for (int64_t c4 = 4 * hl; c4 < kpad; c4 += 64) {
       if (!redo && valid && c4 + 4 <= d) continue;
       uint32_t hw = 0, mw = 0, lw = 0;
 #pragma unroll
@@ -963,7 +954,7 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
             rsum += dr * dr;
           }
         }
-        nsum += (long long)q * q;
+        nsum += (unsigned long long)((long long)q * q);
         const uint32_t mq = (q >> kLimb) & ((1 << kLimb) - 1), lq = q & ((1 << kLimb) - 1);
         msq += mq * mq;
         lsq += lq * lq;
@@ -971,39 +962,30 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
         mw |= mq << (8 * j);
         lw |= lq << (8 * j);
       }
-      *reinterpret_cast<uint32_t*>(hrow + c4) = hw;
-      *reinterpret_cast<uint32_t*>(mrow + c4) = mw;
-      *reinterpret_cast<uint32_t*>(lrow + c4) = lw;
+      *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
+      *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
+      *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
     }
-    if (BULK) {
-      // every warp is done with this stage: refill it
-      __syncthreads();
-      if (threadIdx.x == 0 && i + n_stages < n_it) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(i + n_stages, slot);
-      }
-      if (++slot == n_stages) slot = 0, phase ^= 1u;
+    // every half-warp is done with this stage: refill it
+    __syncthreads();
+    if (threadIdx.x == 0 && i + n_stages < n_it) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + n_stages, slot);
     }
-    // row sums: 32-bit limb norms by REDUX; sum q^2 (< 2^63) in three 21-bit
-    // chunks by REDUX; the fp64 sums by shuffles
-    msq = __reduce_add_sync(0xffffffffu, msq);
-    lsq = __reduce_add_sync(0xffffffffu, lsq);
-    {
-      const unsigned long long u = (unsigned long long)nsum;  // per lane < 2^55
-      const unsigned long long c0 = __reduce_add_sync(0xffffffffu, (unsigned)(u & 0x1fffff));
-      const unsigned long long c1 =
-          __reduce_add_sync(0xffffffffu, (unsigned)((u >> 21) & 0x1fffff));
-      const unsigned long long c2 = __reduce_add_sync(0xffffffffu, (unsigned)(u >> 42));
-      nsum = (long long)(c0 + (c1 << 21) + (c2 << 42));
-    }
-    for (int o = 16; o; o >>= 1) {
+    if (++slot == n_stages) slot = 0, phase ^= 1u;
+    // row sums over the 16 lanes of the half-warp
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
       esum += __shfl_xor_sync(0xffffffffu, esum, o);
       ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
       rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+      nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      msq += __shfl_xor_sync(0xffffffffu, msq, o);
+      lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
     }
-    if (lane == 0) {
-      nq[p] = nsum;
-      cq[p] = (int32_t)(nsum >> kYShift);
+    if (hl == 0) {
+      nq[p] = (int64_t)nsum;
+      cq[p] = (int32_t)((int64_t)nsum >> kYShift);
       w_m = max(w_m, (unsigned long long)msq);  // pads are all-zero rows
       w_l = max(w_l, (unsigned long long)lsq);
       if (valid) {
@@ -1025,17 +1007,18 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
       // bounds every row's |x - c - s q| (the fp64 evaluation of each
       // coordinate of e is off by <= 3.1u|y_k|, u = 2^-53), and
       // sqrt(max rsum) is the max row distance to the tile centre.
-      if (lane == 0) {
-        s_red[0][warp] = w_m, s_red[1][warp] = w_l;
-        s_red[2][warp] = w_valid ? w_e + 1 : 0;  // +1: nonzero marks "has valid rows"
-        s_red[3][warp] = w_y;
-        s_red[4][warp] = w_r;
+      if (hl == 0) {
+        const int h2 = 2 * warp + half;
+        s_red[0][h2] = w_m, s_red[1][h2] = w_l;
+        s_red[2][h2] = w_valid ? w_e + 1 : 0;  // +1: nonzero marks "has valid rows"
+        s_red[3][h2] = w_y;
+        s_red[4][h2] = w_r;
       }
       __syncthreads();
       if (threadIdx.x < 5) {
         unsigned long long m = 0;
 #pragma unroll
-        for (int w = 0; w < kQWarps; ++w) m = max(m, s_red[threadIdx.x][w]);
+        for (int w = 0; w < 2 * kQWarps; ++w) m = max(m, s_red[threadIdx.x][w]);
         s_red[threadIdx.x][0] = m;
       }
       __syncthreads();
@@ -1407,28 +1390,20 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   {
     const int64_t stage = (int64_t)kQRows * d * 8;
     const int n_stages = (int)std::min<int64_t>(kQMaxStages, (kQSmem - 16 * d) / stage);
-    auto args = [&](auto kern, unsigned grid, size_t smem) {
-      kern<<<grid, 256, smem, stream>>>(
-          Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
-          reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P),
-          tp->s_te.as<unsigned long long>(), cen, reinterpret_cast<unsigned long long*>(rad),
-          tp->s_lim.as<uint32_t>(), n_stages);
-    };
-    if (n_stages >= 2) {
-      static bool attr = false;
-      if (!attr) {
-        BM_CHECK_CUDA(cudaFuncSetAttribute(quantize_kernel<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem));
-        attr = true;
-      }
-      const size_t smem = (size_t)n_stages * stage + 16 * d;  // ring + two centres
-      const int per_sm = std::max<int>(1, std::min<int>(3, (int)((220 * 1024) / smem)));
-      args(quantize_kernel<true>,
-           (unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * per_sm), smem);
-    } else {
-      args(quantize_kernel<false>, (unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * 8),
-           0);
+    BM_REQUIRE(n_stages >= 2, "quantiser ring: d=%lld too large", (long long)d);
+    static bool attr = false;
+    if (!attr) {
+      BM_CHECK_CUDA(cudaFuncSetAttribute(quantize_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem));
+      attr = true;
     }
+    const size_t smem = (size_t)n_stages * stage + 16 * d;  // ring + two centres
+    const int per_sm = std::max<int>(1, std::min<int>(3, (int)((220 * 1024) / smem)));
+    quantize_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * per_sm), 256, smem,
+                      stream>>>(
+        Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
+        reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
+        cen, reinterpret_cast<unsigned long long*>(rad), tp->s_lim.as<uint32_t>(), n_stages);
     BM_CHECK_LAUNCH();
   }
   BM_TRY(make_qmap(&tp->qmap, tp->s_pl.ptr, P, kpad));

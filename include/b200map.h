@@ -203,7 +203,9 @@ int bm_group_nodes(const int64_t* d_rows, const int64_t* h_offsets, int64_t n_el
  * overlapping_pairs candidates (cover.py:74-81) because a shared row implies
  * overlapping elements. n_points bounds the row ids.
  * Call with d_edges == NULL to get the count in *h_n_edges (synchronises);
- * then again with d_edges (3 * n_edges int64, row-major s,t,w). */
+ * then again with d_edges (3 * n_edges int64, row-major s,t,w). A d_edges
+ * buffer of n_nodes * (n_nodes - 1) / 2 edges always suffices, so one call
+ * with such a buffer both counts and writes. */
 int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_offsets,
                    int64_t n_nodes, int64_t n_points, int64_t* d_edges,
                    int64_t* h_n_edges, void* stream);

@@ -212,6 +212,14 @@ def nerve_edges(node_rows: torch.Tensor, node_off: torch.Tensor, n_nodes: int,
     lib = _native.load()
     s = stream_ptr(node_off.device)
     ne = ctypes.c_int64(0)
+    max_edges = n_nodes * (n_nodes - 1) // 2
+    if 0 < max_edges <= (1 << 22):
+        # a buffer for every possible edge: one call computes and writes them
+        edges = torch.empty((max_edges, 3), dtype=torch.int64, device=node_off.device)
+        rc = lib.bm_nerve_edges(P(node_rows), P(node_off), n_nodes, n_points, P(edges),
+                                ctypes.byref(ne), s)
+        _native.check(rc, "nerve edges")
+        return edges[: ne.value].cpu().numpy()
     rc = lib.bm_nerve_edges(P(node_rows), P(node_off), n_nodes, n_points, None,
                             ctypes.byref(ne), s)
     _native.check(rc, "nerve edges (count)")

@@ -412,9 +412,10 @@ def main():
                      "kernel_share_of_step": adj_s / (t_dev / args.steps),
                      "alg_flops_per_step": F_exec, "alg_flops_unpruned_per_step": F,
                      "tile_pairs_pruned_frac": tiles_skip / max(tiles_tot, 1),
-                     # exactness costs 6 int8 limb products per pair (each int8 MAC at
-                     # twice the bf16 rate): the formulation's ceiling is 1/3 of peak
-                     "ceiling_frac_exact_int8": 1.0 / 3.0,
+                     # exactness costs 6 int8 limb products per credited pair: at
+                     # the nominal dense int8 rate (4.5 POPS, B200_PROFILING.md) the
+                     # formulation tops out at 750 credited TFLOP/s
+                     "ceiling_frac_exact_int8": (4500.0 / 6.0) / peak,
                      "peak_source": f"{src} bf16 sustained"},
         "gpu_launches": int(launches),
         "nodes": int(g.n_nodes), "edges": int(len(g.edges)),

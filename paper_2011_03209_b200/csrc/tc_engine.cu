@@ -605,15 +605,21 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         mbar_wait(acc_full + 0, ph_acc[0]);
         EP_MARK(0);
         tc_fence_after();
+        static_assert(kEpiCols == 32, "two 16-column TMEM loads per accumulator");
         int32_t t1[kEpiCols];
-#pragma unroll
-        for (int h = 0; h < kEpiCols / 16; ++h) {
-          int32_t x0[16], x1[16];
-          tmem_ld16(tq + 0 * kBN + h * 16, x0);
-          tmem_ld16(tq + 1 * kBN + h * 16, x1);
+        {
+          // all four loads in flight, one wait: A0/A1 are released sooner
+          int32_t x0a[16], x0b[16], x1a[16], x1b[16];
+          tmem_ld16(tq + 0 * kBN, x0a);
+          tmem_ld16(tq + 0 * kBN + 16, x0b);
+          tmem_ld16(tq + 1 * kBN, x1a);
+          tmem_ld16(tq + 1 * kBN + 16, x1b);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) t1[h * 16 + j] = x0[j] * (1 << kLimb) + x1[j];
+          for (int j = 0; j < 16; ++j) {
+            t1[j] = x0a[j] * (1 << kLimb) + x1a[j];
+            t1[16 + j] = x0b[j] * (1 << kLimb) + x1b[j];
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -624,13 +630,16 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         mbar_wait(acc_full + 1, ph_acc[1]);
         EP_MARK(1);
         tc_fence_after();
-#pragma unroll
-        for (int h = 0; h < kEpiCols / 16; ++h) {
-          int32_t a2[16];
-          tmem_ld16(tq + 2 * kBN + h * 16, a2);
+        {
+          int32_t a2a[16], a2b[16];
+          tmem_ld16(tq + 2 * kBN, a2a);
+          tmem_ld16(tq + 2 * kBN + 16, a2b);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) t1[h * 16 + j] += a2[j] >> kLimb;
+          for (int j = 0; j < 16; ++j) {
+            t1[j] += a2a[j] >> kLimb;
+            t1[16 + j] += a2b[j] >> kLimb;
+          }
         }
         tc_fence_before();
         __syncwarp();

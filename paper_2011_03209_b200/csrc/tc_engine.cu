@@ -511,21 +511,22 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       mbar_wait(a_empty, a_empty_ph ^ 1);
       a_empty_ph ^= 1;
       tc_fence_after();
-      for (int pl = 0; pl < 2; ++pl) {
-        const uint4* src = reinterpret_cast<const uint4*>(P.planes + (int64_t)pl * P.P * kpad +
-                                                           prow * kpad);
-        for (int c0 = 0; c0 < kpad / 4; c0 += 32) {
-          uint32_t v[32];
+      // both planes' chunk loads in flight together: half the dependent
+      // global round trips per unit (the MMA warp waits on this at unit
+      // boundaries)
+      const uint4* srcH = reinterpret_cast<const uint4*>(P.planes + prow * kpad);
+      const uint4* srcM = reinterpret_cast<const uint4*>(P.planes + P.P * kpad + prow * kpad);
+      for (int c0 = 0; c0 < kpad / 4; c0 += 32) {
+        uint32_t vh[32], vm[32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint4 w = __ldg(src + c0 / 4 + i);
-            v[4 * i] = w.x;
-            v[4 * i + 1] = w.y;
-            v[4 * i + 2] = w.z;
-            v[4 * i + 3] = w.w;
-          }
-          tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + pl * ncol_plane + c0, v);
+        for (int i = 0; i < 8; ++i) {
+          const uint4 w = __ldg(srcH + c0 / 4 + i);
+          const uint4 x = __ldg(srcM + c0 / 4 + i);
+          vh[4 * i] = w.x, vh[4 * i + 1] = w.y, vh[4 * i + 2] = w.z, vh[4 * i + 3] = w.w;
+          vm[4 * i] = x.x, vm[4 * i + 1] = x.y, vm[4 * i + 2] = x.z, vm[4 * i + 3] = x.w;
         }
+        tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + c0, vh);
+        tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + ncol_plane + c0, vm);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();

@@ -647,7 +647,10 @@ __global__ void emit_tiles_kernel(ElemTables et, const int32_t* __restrict__ row
 
 // tensor-core work units hold up to kTcUnit column tiles (the row tile's A
 // operand is loaded once per unit)
-constexpr int kTcUnit = 16;
+#ifndef BM_TC_UNIT
+#define BM_TC_UNIT 16
+#endif
+constexpr int kTcUnit = BM_TC_UNIT;
 
 // unit counts per row tile (from the kept slots of consecutive rows)
 __global__ void unit_counts_kernel(const int64_t* __restrict__ row_first, int64_t n_rt,
@@ -1060,6 +1063,12 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           uint32_t m = bits[r * 4 + w] & (DIAG ? coreI[w] : coreJ[w]);
+          if (DIAG) {
+            // the diagonal tile is symmetric (the ε relation is): row r joins
+            // only its neighbours c < r, each edge is visited once
+            const int lo = r - w * 32;
+            m &= lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : (1u << lo) - 1u);
+          }
           while (m) {
             const int c = w * 32 + __ffs(m) - 1;
             m &= m - 1;

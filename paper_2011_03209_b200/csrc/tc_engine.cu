@@ -386,8 +386,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     // ------------------------------------------------------------ producer (TMA)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qmap) : "memory");
-      uint32_t stage = 0, ph_empty[kStages] = {0, 0}, a_empty_ph = 0;
-      uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
+      // per-slot phases as bit masks (a dynamically indexed array would live in local memory)
+      uint32_t stage = 0, ph_empty = 0, a_empty_ph = 0;
+      uint32_t islot = 0, ph_info = 0;
       for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
         const TileUnit un = P.units[u];
         const int pb = P.et.pbase[un.k];
@@ -402,15 +403,15 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         for (int t = 0; t < un.cnt; ++t) {
           const int b = P.tiles[un.off + t].J;
           // tile info for the epilogue (runs ahead by up to kInfo tiles)
-          mbar_wait(info_empty + islot, ph_info[islot] ^ 1);
-          ph_info[islot] ^= 1;
+          mbar_wait(info_empty + islot, ((ph_info >> islot) & 1u) ^ 1u);
+          ph_info ^= 1u << islot;
           info[islot].th = *reinterpret_cast<const int2*>(P.thr + (un.off + t - P.slot0));
           info[islot].J = b;
           mbar_expect_tx(info_full + islot, kBN * 4);
           bulk_load(info[islot].cq, P.cq + pb + b * kBN, kBN * 4, info_full + islot);
           islot = (islot + 1) % kInfo;
-          mbar_wait(b_empty + stage, ph_empty[stage] ^ 1);
-          ph_empty[stage] ^= 1;
+          mbar_wait(b_empty + stage, ((ph_empty >> stage) & 1u) ^ 1u);
+          ph_empty ^= 1u << stage;
           mbar_expect_tx(b_full + stage, b_bytes);
           uint8_t* dst = sB + stage * b_bytes;
           for (int pl = 0; pl < 3; ++pl)
@@ -434,7 +435,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     constexpr uint32_t NCOL_PLANE = NKC * 32;          // TMEM columns per limb plane
     constexpr uint32_t BLK = kBN * kKC;                // bytes of one (plane, K-chunk) block
     constexpr uint32_t BPLANE = NKC * BLK;
-    uint32_t a_ph = 0, stage = 0, ph_full[kStages] = {0, 0};
+    uint32_t a_ph = 0, stage = 0, ph_full = 0;  // per-stage phase bits
     uint32_t ph_acc[2] = {0, 0};
     const uint32_t aH = tmem_base, aM = tmem_base + NCOL_PLANE;
     const uint64_t aL_desc = smem_desc(smem_u32(sAL));
@@ -451,9 +452,9 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
       tc_fence_after();
       for (int t = 0; t < un.cnt; ++t) {
         tw = clock64();
-        mbar_wait(b_full + stage, ph_full[stage]);
+        mbar_wait(b_full + stage, (ph_full >> stage) & 1u);
         prof_b += clock64() - tw;
-        ph_full[stage] ^= 1;
+        ph_full ^= 1u << stage;
         const uint64_t bd = b_desc0 + ((stage * 3 * BPLANE) >> 4);
         // descriptor of (B plane pl, K-step ks): start address advances in 16-byte units
 #define BDESC(pl, ks) (bd + ((uint64_t)((pl) * BPLANE + ((ks) >> 2) * BLK + ((ks) & 3) * 32) >> 4))
@@ -553,7 +554,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     const int ch = ew >> 2;
     const int row = q * 32 + lane;
     uint32_t ph_acc[2] = {0, 0};
-    uint32_t islot = 0, ph_info[kInfo] = {0, 0, 0};
+    uint32_t islot = 0, ph_info = 0;  // per-slot phase bits
 #ifdef BM_TC_PROFILE
     long long ep[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long ep_t0 = clock64();
@@ -587,8 +588,8 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         // r = floor(N_i/U) + per-tile constant (tile_thr_kernel, with the
         // margins that absorb every rounding).
         EP_START();
-        mbar_wait(info_full + islot, ph_info[islot]);
-        ph_info[islot] ^= 1;
+        mbar_wait(info_full + islot, (ph_info >> islot) & 1u);
+        ph_info ^= 1u << islot;
         const int2 th = info[islot].th;
         const int J = info[islot].J;
         const int col0 = J * kBN + ch * kEpiCols;     // first local column of this warp

@@ -1068,6 +1068,15 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
             // only its neighbours c < r, each edge is visited once
             const int lo = r - w * 32;
             m &= lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : (1u << lo) - 1u);
+          } else if (m && rmm[2][w] == rmm[3][w]) {
+            // every core column of word w has the same global root (warp w's
+            // min == max): one join with the first neighbour stands for all
+            const int gn = rmm[2][w];
+            if (gn != gr && gn != last) {
+              last = gn;
+              if (lunion(lp, r, kTile + w * 32 + __ffs(m) - 1)) any_merge = 1;
+            }
+            continue;
           }
           while (m) {
             const int c = w * 32 + __ffs(m) - 1;

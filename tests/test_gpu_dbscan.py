@@ -189,3 +189,37 @@ def test_degenerate_inputs(engine, case):
         out = run(X, rows, eps, 4, order=order, engine=engine)
         clusters, noise = O.dbscan_element(X, rows, eps, 4, order)
         assert out.clusters == clusters and out.noise == noise, (case, order)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("layout", ["blobs", "chains"])
+def test_many_components_across_tiles(engine, layout):
+    """Many components per 128-row tile, joined across tiles: hundreds of tight
+    blobs, or long chains whose links only exist between consecutive points
+    (the union-find shortcuts for symmetric diagonal tiles and single-root
+    column words must not lose a join)."""
+    from paper_2011_03209_b200 import DbscanParams, DistanceStrategy, cluster_all, from_array
+
+    rng = np.random.default_rng(11 if layout == "blobs" else 12)
+    d = 40
+    if layout == "blobs":
+        centres = rng.uniform(-50.0, 50.0, (300, d))
+        X = np.repeat(centres, 8, axis=0) + 0.05 * rng.standard_normal((2400, d))
+        eps = 0.6
+    else:
+        starts = rng.uniform(-50.0, 50.0, (12, d))
+        dirs = rng.standard_normal((12, d))
+        dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+        steps = np.arange(200)[:, None]
+        X = np.concatenate([s + 0.4 * steps * u for s, u in zip(starts, dirs)])
+        X += 0.01 * rng.standard_normal(X.shape)
+        eps = 0.45
+    X = X[rng.permutation(len(X))]
+    members = [np.arange(len(X)), np.sort(rng.choice(len(X), 1500, replace=False))]
+    for min_pts in (2, 3):
+        cl = cluster_all(from_array(X), members, DbscanParams(eps, min_pts),
+                         DistanceStrategy(threshold=10 ** 9), engine=engine)
+        for k, m in enumerate(members):
+            clusters, noise = O.dbscan_element(X, m, eps, min_pts, O.ORDER_SEQUENTIAL)
+            assert len(clusters) > 10
+            assert cl[k].clusters == clusters and cl[k].noise == noise, (layout, k, min_pts)

@@ -224,8 +224,10 @@ int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_offsets,
  *   h_comp/h_comp_off       per node, the JSON text of its composition object
  * Call with out == NULL to get the length in *h_len, then with a buffer of at
  * least that many bytes: when the second call comes from the same thread with
- * the same arguments (and unchanged inputs) it copies the text formatted by
- * the first instead of formatting again. */
+ * the same arguments it copies the text formatted by the first instead of
+ * formatting again. The cache is keyed on the pointers and sizes only, so the
+ * caller must not modify the input arrays in place between the sizing call
+ * and the writing call (a changed input needs a fresh sizing call). */
 int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows, const int64_t* h_node_off,
                   const int32_t* h_elem, const double* h_stats, int64_t d,
                   const int32_t* h_stat_order, const char* h_names, const int64_t* h_name_off,

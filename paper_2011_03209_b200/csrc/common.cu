@@ -3,6 +3,7 @@
 #include <stdlib.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 
 #include <chrono>
@@ -249,6 +250,20 @@ size_t device_total_bytes() {
   }
   if (dev < 64) cache[dev] = t;
   return t;
+}
+
+int ensure_dyn_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  BM_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, fn);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return BM_OK;
+  BM_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[key] = bytes;
+  return BM_OK;
 }
 
 int num_sms() {

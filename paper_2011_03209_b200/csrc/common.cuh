@@ -51,6 +51,14 @@ void count_launch();
     }                                \
   } while (0)
 
+#define BM_REQUIRE_INTERNAL(cond, ...) \
+  do {                                 \
+    if (!(cond)) {                     \
+      ::bm::set_error(__VA_ARGS__);    \
+      return BM_ERR_INTERNAL;          \
+    }                                  \
+  } while (0)
+
 #define BM_TRY(expr)        \
   do {                      \
     int _rc = (expr);       \
@@ -117,6 +125,11 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Number of SMs on the current device (cached per device).
 int num_sms();
+// Opt the kernel `fn` into `bytes` of dynamic shared memory on the CURRENT
+// device. The attribute is per (device context, function), so the guard is
+// keyed on both and taken under a lock (re-entrant ABI calls from several
+// host threads, and one process driving several GPUs).
+int ensure_dyn_smem(const void* fn, int bytes);
 // Total memory of the current device (cached per device).
 size_t device_total_bytes();
 

@@ -1146,6 +1146,43 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
   }
 }
 
+// Debug check (B200MAP_CHECK_SYMMETRY=1): every diagonal tile bitmap equals
+// its transpose. The diagonal components pass joins only the bits c < r of
+// row r, so it relies on this invariant: the eps relation is symmetric, and
+// every engine must produce (r, c) and (c, r) alike (the tensor-core epilogue
+// reaches them by different routes: per-row bounds, floor(N_j / U) on the
+// column side, the recheck queue; each route is rigorous, hence they agree).
+__global__ void __launch_bounds__(128)
+diag_symmetry_kernel(const uint32_t* __restrict__ adj, const TileUnit* __restrict__ units,
+                     const TileRef* __restrict__ tiles, int64_t slot0, int64_t n_units,
+                     unsigned long long* __restrict__ bad) {
+  __shared__ uint32_t bits[kTileWords];
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const TileUnit un = units[u];
+    for (int s = 0; s < un.cnt; ++s) {
+      const int64_t g = un.off + s;
+      if (tiles[g].J != un.I) continue;  // block-uniform
+      __syncthreads();
+      reinterpret_cast<uint4*>(bits)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(adj + (g - slot0) * kTileWords)[threadIdx.x];
+      __syncthreads();
+      const int r = threadIdx.x;
+      int nbad = 0;
+      for (int c = 0; c < kTile; ++c) {
+        const uint32_t a = (bits[r * 4 + (c >> 5)] >> (c & 31)) & 1u;
+        const uint32_t b = (bits[c * 4 + (r >> 5)] >> (r & 31)) & 1u;
+        nbad += a != b;
+      }
+      if (nbad) atomicAdd(bad, (unsigned long long)nbad);
+    }
+  }
+}
+
+bool check_symmetry() {
+  const char* e = getenv("B200MAP_CHECK_SYMMETRY");
+  return e && e[0] == '1';
+}
+
 // per 128-row tile: the common root of its rows if every valid row is core
 // and all share one root (stale roots are fine: still in the component), else -1
 __global__ void tile_uniform_kernel(ElemTables et, int64_t n_rt, const uint8_t* __restrict__ core,
@@ -1247,13 +1284,7 @@ template <int DEPTH>
 int launch_exact_depth(const double* Xg, int64_t d, const ElemTables& et, const TileRef* tiles,
                        int64_t n_tiles, double eps, uint32_t* adj, int32_t* nonempty,
                        const PwProgram& prog, cudaStream_t stream) {
-  static bool attr_done = false;  // per process; attribute is per function
-  if (!attr_done) {
-    BM_CHECK_CUDA(cudaFuncSetAttribute(adjacency_exact_kernel<DEPTH>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kExactSmem));
-    attr_done = true;
-  }
+  BM_TRY(ensure_dyn_smem((const void*)adjacency_exact_kernel<DEPTH>, (int)kExactSmem));
   const int64_t kMaxGrid = 1ll << 30;
   for (int64_t t0 = 0; t0 < n_tiles; t0 += kMaxGrid) {
     int64_t nb = std::min<int64_t>(kMaxGrid, n_tiles - t0);
@@ -1311,9 +1342,15 @@ struct WindowBufs {
   int64_t slot0 = 0, n_tiles = 0, n_diag = 0, n_off = 0, n_tc = 0, pairs = 0;
 };
 
-bool prune_enabled(int64_t d) {
+// eps outside [1e-140, 1e140]: squared differences near eps can underflow
+// to subnormals or overflow, where the relative error model behind the
+// pruning bound (and the tensor-core band) does not hold — every tile pair is
+// computed and every tensor-core decision is rechecked in exact fp64.
+bool eps_in_model(double eps) { return eps >= 1e-140 && eps <= 1e140; }
+
+bool prune_enabled(int64_t d, double eps) {
   const char* e = getenv("B200MAP_NO_PRUNE");  // tests: identity order, every tile pair
-  return !(e && e[0] == '1') && d <= 512;
+  return !(e && e[0] == '1') && d <= 512 && eps_in_model(eps);
 }
 
 struct BatchCtx {
@@ -1402,7 +1439,7 @@ struct BatchCtx {
     inv = ent + P;
     et = ElemTables{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, ent, nb_el};
     const int64_t* rows_b = d_rows + h_offsets[k0];
-    const bool prune = prune_enabled(d);
+    const bool prune = prune_enabled(d, eps);
 
     trace_mark("setup:tables", stream);
     // ---- row order inside each element: grouped (stable by seed) or identity
@@ -1695,6 +1732,18 @@ struct BatchCtx {
     WindowBufs w;
     BM_TRY(window(I0, I1, w));
     int32_t* nonempty = reinterpret_cast<int32_t*>(adj + w.n_tiles * kTileWords);
+    if (w.n_diag > 0 && check_symmetry()) {
+      Scratch s_bad;
+      BM_TRY(scratch_alloc(s_bad, 8, stream));
+      BM_CHECK_CUDA(cudaMemsetAsync(s_bad.ptr, 0, 8, stream));
+      diag_symmetry_kernel<<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
+          adj, w.diag, w.tiles, w.slot0, w.n_diag, s_bad.as<unsigned long long>());
+      BM_CHECK_LAUNCH();
+      unsigned long long h_bad = 0;
+      BM_CHECK_CUDA(cudaMemcpyAsync(&h_bad, s_bad.ptr, 8, cudaMemcpyDeviceToHost, stream));
+      BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+      BM_REQUIRE_INTERNAL(h_bad == 0, "asymmetric diagonal tile bitmap (%llu bits)", h_bad);
+    }
     if (w.n_diag > 0) {
       components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
           adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty);
@@ -1816,6 +1865,9 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
   } else if (engine == BM_ENGINE_AUTO) {
     use_tc = tc_supported(d);
   }
+  // outside the error model every tensor-core decision would be queued for
+  // the exact recheck: run the exact engine directly (same bits)
+  if (!eps_in_model(eps)) use_tc = false;
 
   // ---- batches bounded by the device budget (dense bitmap estimate); an
   //      element whose dense bitmap alone exceeds it is processed by itself in
@@ -2019,6 +2071,7 @@ extern "C" int bm_big_open(const double* d_X, int64_t n, int64_t d, const int64_
   bool use_tc = engine == BM_ENGINE_TC || (engine == BM_ENGINE_AUTO && tc_supported(d));
   BM_REQUIRE(!use_tc || tc_supported(d), "tensor-core engine does not support d=%lld",
              (long long)d);
+  if (!eps_in_model(eps)) use_tc = false;  // see bm_cluster_elements
   BigElement* be = new BigElement();
   be->bc.stream = (cudaStream_t)stream;
   be->bc.d = d;

@@ -185,12 +185,7 @@ pairwise_lens_kernel(const double* __restrict__ X, int64_t d, const int64_t* __r
 template <int MODE>
 int launch_lens(const double* X, int64_t d, const int64_t* q, int64_t nq, const int64_t* tr,
                 int64_t m, const PwLeaf* leaves, double param, double* out, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    BM_CHECK_CUDA(cudaFuncSetAttribute(pairwise_lens_kernel<MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem));
-    attr = true;
-  }
+  BM_TRY(ensure_dyn_smem((const void*)pairwise_lens_kernel<MODE>, (int)kLSmem));
   pairwise_lens_kernel<MODE><<<(unsigned)ceil_div(nq, kLq), 256, kLSmem, s>>>(
       X, d, q, nq, tr, m, leaves, param, out);
   BM_CHECK_LAUNCH();

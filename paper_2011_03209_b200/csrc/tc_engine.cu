@@ -1071,8 +1071,15 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
   }
   if (i < n_el) {
     const double s = scale[i];
-    a_in[i] = __ddiv_rd(__ddiv_rd(eps, 1.0 + gamma), s);
-    a_out[i] = __ddiv_ru(__ddiv_ru(eps, 1.0 - gamma), s);
+    if (eps >= 1e-140 && eps <= 1e140) {
+      a_in[i] = __ddiv_rd(__ddiv_rd(eps, 1.0 + gamma), s);
+      a_out[i] = __ddiv_ru(__ddiv_ru(eps, 1.0 - gamma), s);
+    } else {
+      // squares near eps would underflow/overflow (dbscan.cu eps_in_model):
+      // no certain decision, every pair of the element is rechecked
+      a_in[i] = -1e300;
+      a_out[i] = 1e300;
+    }
   }
 }
 
@@ -1402,12 +1409,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
     const int64_t stage = (int64_t)kQRows * d * 8;
     const int n_stages = (int)std::min<int64_t>(kQMaxStages, (kQSmem - 16 * d) / stage);
     BM_REQUIRE(n_stages >= 2, "quantiser ring: d=%lld too large", (long long)d);
-    static bool attr = false;
-    if (!attr) {
-      BM_CHECK_CUDA(cudaFuncSetAttribute(quantize_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem));
-      attr = true;
-    }
+    BM_TRY(ensure_dyn_smem((const void*)quantize_kernel, kQSmem));
     const size_t smem = (size_t)n_stages * stage + 16 * d;  // ring + two centres
     const int per_sm = std::max<int>(1, std::min<int>(3, (int)((220 * 1024) / smem)));
     quantize_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * per_sm), 256, smem,
@@ -1499,14 +1501,8 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
   BM_TRY(scratch_alloc(s_cnt, 16, stream));
   unsigned long long* d_cnt = s_cnt.as<unsigned long long>();
   const size_t smem = (size_t)nkc * kKC * kBN * (1 + 3 * kStages) + 256 + 1024 + 1600 + 64;
-  static bool attr = false;
-  if (!attr) {
-    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel<1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    BM_CHECK_CUDA(cudaFuncSetAttribute(tc_adjacency_kernel<2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  BM_TRY(ensure_dyn_smem((const void*)tc_adjacency_kernel<1>, 227 * 1024));
+  BM_TRY(ensure_dyn_smem((const void*)tc_adjacency_kernel<2>, 227 * 1024));
   BM_TRY(scratch_alloc(s_tt, (size_t)n_tiles * sizeof(TileThr), stream));
   trace_mark("tc:thr allocated", stream);
   unsigned long long h_cnt[2] = {0, 0};

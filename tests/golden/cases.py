@@ -128,3 +128,65 @@ def pca_fixture_F(X: np.ndarray) -> np.ndarray:
     Xc = X - X.mean(axis=0)
     _, _, vt = np.linalg.svd(Xc[:4000], full_matrices=False)
     return np.ascontiguousarray(Xc @ vt[:2].T)
+
+
+# ---- cfg3-shaped case at the reference's DEFAULT strategy ----------------------
+def cfg3_default():
+    """200k x 256 Gaussian mixture, l2-norm lens, 40 intervals, 30% overlap,
+    eps 21.3, min_pts 5 and the reference's default strategy (precomputed,
+    threshold 20,000, 8 GiB budget): 5 elements exceed 20,000 rows and take the
+    numpy-pairwise (on-the-fly) order (clustering.py:137-139, 201-208), the
+    other 35 the cdist order — both orders at cfg3's dimension and density."""
+    X = gmm(200_000, 256, 10, 5.0, 6)
+    params = dict(filters=[{"kind": "l2-norm"}], n=[40], p=[0.3], eps=21.3, min_pts=5,
+                  norm="none", mode="precomputed", threshold=20_000)
+    return X, params
+
+
+# ---- planted near-eps stress case (256-D, thousands of pairs at +-2 ulp) --------
+def _nudge_to(a, b, eps, cd, max_iter=200):
+    """Move b by single-ulp steps of its largest-difference coordinates until
+    the cdist distance |a - b| lies within 2 ulps of eps (deterministic)."""
+    ulp = np.spacing(eps)
+    order = np.argsort(-np.abs(b - a), kind="stable")
+    for it in range(max_iter):
+        dd = cd(a, b)
+        if abs(dd - eps) <= 2 * ulp:
+            return b, True
+        t = order[it % 16]
+        step = np.nextafter(b[t], np.inf if (b[t] > a[t]) == (dd < eps) else -np.inf)
+        b = b.copy()
+        b[t] = step
+    return b, False
+
+
+def near_eps_case(n_pairs: int = 2400, d: int = 256, eps: float = 3.0, seed: int = 77):
+    """One cover element (column lens, 1 interval) of `n_pairs` planted links
+    whose cdist length is within +-2 ulp of eps; every third link is extended
+    to a chain a-b-c (both links planted). Anchors are ~68 apart, so cross
+    distances are far from eps and most tile pairs are pruned while the
+    planted ones are not. min_pts = 2: each link's eps decision alone decides
+    whether its points form a cluster, in both summation orders (which
+    disagree on some links)."""
+    from scipy.spatial.distance import cdist
+
+    def cd(u, v):
+        return float(cdist(u[None], v[None])[0, 0])
+
+    rng = np.random.default_rng(seed)
+    pts = []
+    for m in range(n_pairs):
+        a = 3.0 * rng.standard_normal(d)
+        chain = [a]
+        for _ in range(2 if m % 3 == 0 else 1):
+            u = rng.standard_normal(d)
+            u /= np.sqrt((u * u).sum())
+            b = chain[-1] + eps * u
+            b, _ = _nudge_to(chain[-1], b, eps, cd)
+            chain.append(b)
+        pts.extend(chain)
+    X = np.vstack(pts)
+    X = X[rng.permutation(len(X))]  # links spread across tiles and entry order
+    params = dict(filters=[{"kind": "column", "column": "x1"}], n=[1], p=[0.0], eps=eps,
+                  min_pts=2, norm="none", mode="precomputed", threshold=20_000)
+    return X, params

@@ -65,7 +65,38 @@ def as_u8(b: bytes):
     return np.frombuffer(b, dtype=np.uint8)
 
 
+def near_eps():
+    """Planted near-eps links in 256-D (cases.near_eps_case), both modes."""
+    X, p = cases.near_eps_case()
+    pre = run(X, dict(p, mode="precomputed"))
+    fly = run(X, dict(p, mode="on-the-fly"))
+    assert pre != fly, "near-eps case does not separate the strategy modes"
+    save("near_eps", x_sha=np.array(cases.sha(X)), **compact("pre", pre), **compact("fly", fly))
+
+
+def compact(prefix, graph_bytes):
+    """A large graph JSON as its sha256 plus node rows and edges (the JSON
+    carries 256 column means per node; the hash pins every byte of it)."""
+    import hashlib
+    import json
+
+    g = json.loads(graph_bytes)
+    rows = [nd["rows"] for nd in g["nodes"]]
+    return {f"{prefix}_sha": np.array(hashlib.sha256(graph_bytes).hexdigest()),
+            f"{prefix}_node_off": np.cumsum([0] + [len(r) for r in rows]).astype(np.int64),
+            f"{prefix}_node_rows": (np.concatenate([np.asarray(r, dtype=np.int32) for r in rows])
+                                    if rows else np.zeros(0, np.int32)),
+            f"{prefix}_edges": np.array([(e["s"], e["t"], e["w"]) for e in g["edges"]],
+                                        dtype=np.int64).reshape(-1, 3)}
+
+
 def main():
+    if len(sys.argv) > 1:  # named pieces only, e.g. `make_golden.py near_eps`
+        for name in sys.argv[1:]:
+            t = time.time()
+            globals()[name]()
+            print(name, time.time() - t)
+        return
     threads = os.cpu_count() or 1
     t = time.time()
     X, p = cases.cfg1()
@@ -102,6 +133,7 @@ def main():
     g = build_graph(cl, pc, fv, cover, manifest={"test": True})
     save("pca2d", graph=as_u8(graph_to_json(g)), F=F, x_sha=np.array(cases.sha(X)),
          sizes=np.array([m.size for m in members]))
+    near_eps()
 
 
 if __name__ == "__main__":

@@ -1,7 +1,10 @@
 """GPU, full size: the headline configuration (cfg3: 1M x 256, 40 intervals,
-eps 21.3) checked through size-independent properties, since the reference
-itself needs hours here.
+eps 21.3; the reference itself needs hours here).
 
+* every node's rows and every edge equal the full-size golden
+  (tests/golden/cfg3_full.npz: scipy cdist over every pair of every element,
+  chunked oracle, make_golden_cfg3.py);
+* the pruned build equals the build over every tile pair (pruning soundness);
 * the tensor-core engine and the all-fp64 engine (parity-pinned against the
   oracle at small sizes) build identical graphs: every node's rows and every
   edge;
@@ -38,8 +41,18 @@ def cfg3_graphs():
     Xd = to_device_f64(X, dev)
     pc = from_array(X)
     out = {}
-    for engine in (2, 1):
-        g = build_device(Xd, pc, params, 1 << 62, None, engine)
+    import os
+
+    for engine in (2, 1, "noprune"):
+        if engine == "noprune":  # tensor-core engine over EVERY tile pair
+            os.environ["B200MAP_NO_PRUNE"] = "1"
+        if engine == 2:  # the library checks every diagonal tile's symmetry
+            os.environ["B200MAP_CHECK_SYMMETRY"] = "1"
+        try:
+            g = build_device(Xd, pc, params, 1 << 62, None, 2 if engine == "noprune" else engine)
+        finally:
+            os.environ.pop("B200MAP_NO_PRUNE", None)
+            os.environ.pop("B200MAP_CHECK_SYMMETRY", None)
         out[engine] = dict(
             node_rows=g.node_rows.cpu().numpy(), node_off=g.node_off.cpu().numpy(),
             node_elem=np.asarray(g.node_elem), edges=np.asarray(g.edges),
@@ -55,6 +68,34 @@ def test_cfg3_engines_identical(cfg3_graphs):
     for key in ("node_rows", "node_off", "node_elem", "edges", "sizes"):
         assert np.array_equal(a[key], b[key]), key
     assert len(a["node_off"]) - 1 > 100  # a non-degenerate graph
+
+
+def test_cfg3_pruning_sound_at_full_size(cfg3_graphs):
+    """The pruned build equals the build that computes every tile pair of
+    every element (B200MAP_NO_PRUNE=1: identity row order, 3.2e13 flop of
+    distance tiles): pruning removes no eps-pair at the headline size."""
+    _, _, out = cfg3_graphs
+    a, b = out[2], out["noprune"]
+    for key in ("node_rows", "node_off", "node_elem", "edges", "sizes"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+def test_cfg3_equals_full_size_golden(cfg3_graphs, golden):
+    """Every node's rows and every edge of the headline graph equal the
+    golden made by the chunked oracle (scipy cdist itself over every pair of
+    every element, union-find semantics of clustering.py:151-198; pinned to
+    the reference's own goldens in test_oracle.py). make_golden_cfg3.py."""
+    X, _, out = cfg3_graphs
+    z = golden("cfg3_full")
+    import hashlib
+
+    assert hashlib.sha256(X.tobytes()).hexdigest() == str(z["x_sha"])
+    g = out[2]
+    assert np.array_equal(g["sizes"], z["sizes"])
+    assert np.array_equal(g["node_off"], z["node_off"])
+    assert np.array_equal(g["node_rows"], z["node_rows"].astype(np.int64))
+    assert np.array_equal(g["node_elem"], z["node_elem"])
+    assert np.array_equal(g["edges"].reshape(-1, 3), z["edges"])
 
 
 def test_cfg3_lens_and_membership_bitwise(cfg3_graphs):
@@ -202,3 +243,20 @@ def test_cfg4_pca_grid_library_pieces():
             _check_sampled(X, w, g, k, rows, got, rng, n_sample=8)
             checked_large += 1
     assert checked_small >= 5 and checked_large >= 5
+
+
+def test_cfg3_default_strategy_bytes(golden):
+    """A cfg3-shaped 200k x 256 cloud at the reference's DEFAULT strategy
+    (threshold 20,000): 5 elements of 20-22k rows run in numpy's pairwise
+    order, 35 in cdist order. The graph JSON (sha256 of every byte) equals the
+    one nervemap itself produced (make_golden_cfg3d.py)."""
+    import hashlib
+
+    import cases
+    from test_gpu_pipeline import graph_bytes
+
+    z = golden("cfg3d")
+    X, p = cases.cfg3_default()
+    assert cases.sha(X) == str(z["x_sha"])
+    got = graph_bytes(X, p)
+    assert hashlib.sha256(got).hexdigest() == str(z["graph_sha"])

@@ -55,12 +55,20 @@ def parse():
 def workload_params(w):
     from paper_2011_03209_b200 import DistanceStrategy, FilterSpec, MapperParams
 
-    filters = [FilterSpec(kind=k, column=c) if k == "column" else FilterSpec(kind=k)
-               for k, c in w.lens]
+    if is_pca(w):  # lens supplied as FilterValues (the specs only label the axes)
+        filters = [FilterSpec(kind="l2-norm")] * 2
+    else:
+        filters = [FilterSpec(kind=k, column=c) if k == "column" else FilterSpec(kind=k)
+                   for k, c in w.lens]
     # the 1M-row configs are run with matrices for every
-    # element on both sides (threshold >= max n_k), i.e. the cdist order.
+    # element on both sides (threshold >= max n_k), i.e. the cdist order;
+    # cfg3d keeps the reference's default threshold (20,000)
     return MapperParams(filters=filters, n=list(w.intervals), p=list(w.overlaps), eps=w.eps,
-                        min_pts=w.min_pts, strategy=DistanceStrategy(threshold=10 ** 9))
+                        min_pts=w.min_pts, strategy=DistanceStrategy(threshold=w.threshold))
+
+
+def is_pca(w):
+    return tuple(w.lens) == ("pca2",)
 
 
 BUDGET = 1 << 62
@@ -169,7 +177,12 @@ FULL_BUILD_CONFIGS = ("cfg1", "cfg2")
 def host_members(X, w):
     from oracle import mapper_oracle as O
 
-    F = np.column_stack([O.lens(X, k, int(c[1:]) if c else 0) for k, c in w.lens])
+    if is_pca(w):
+        from paper_2011_03209_b200 import workloads
+
+        F = workloads.pca2_lens(X)
+    else:
+        F = np.column_stack([O.lens(X, k, int(c[1:]) if c else 0) for k, c in w.lens])
     axes = [O.cover_axis(F[:, a], w.intervals[a], w.overlaps[a]) for a in range(F.shape[1])]
     return O.membership(F, axes)
 
@@ -205,7 +218,9 @@ class RefSampler:
         self.members = host_members(X, w)  # lens + cover + membership at full size
         self.t_lens_cover = _t.perf_counter() - t0
         self.sizes = np.array([len(m) for m in self.members], dtype=np.int64)
-        self.orders = [O.ORDER_SEQUENTIAL] * len(self.members)  # threshold >= max n_k
+        # the reference's per-element order choice (clustering.py:201-208)
+        self.orders = [O.element_order(int(s), "precomputed", w.threshold, BUDGET)
+                       for s in self.sizes]
         self.rows = np.zeros(len(self.members))
         self.secs = np.zeros(len(self.members))
         self.wall = 0.0
@@ -260,7 +275,7 @@ def full_build_baseline(w, workers):
 
     X = workloads.points(w)
     r = RT.full_build(X, ref_lenses(w), list(w.intervals), list(w.overlaps), w.eps,
-                      w.min_pts, workers=workers)
+                      w.min_pts, threshold=w.threshold, budget=BUDGET, workers=workers)
     r.update(config=w.name, points=w.n, points_per_s=w.n / r["seconds"])
     return r
 
@@ -335,11 +350,30 @@ def run_reference(args, w, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def library_pieces(Xnp, Fnp, w, params):
+    """cfg4's reference-facing path: the library pieces on host inputs."""
+    from paper_2011_03209_b200 import (DbscanParams, FilterValues, build_cover, build_graph,
+                                       cluster_all, from_array, graph_to_json, membership)
+
+    pc = from_array(Xnp)
+    fv = FilterValues(values=Fnp, specs=list(params.filters))
+    cover = build_cover(fv, list(w.intervals), list(w.overlaps))
+    members = membership(fv, cover)
+    cl = cluster_all(pc, members, DbscanParams(w.eps, w.min_pts), params.strategy,
+                     budget_bytes=BUDGET)
+    g = build_graph(cl, pc, fv, cover, manifest=params.manifest())
+    graph_to_json(g)
+    return g
+
+
 def config_of(w, world):
     return {"workload": f"{w.name}: {w.n}x{w.d} Gaussian mixture (K={w.k}, box={w.box}, "
                         f"seed={w.seed}), lens={list(w.lens)}, intervals={list(w.intervals)}, "
                         f"overlap={list(w.overlaps)}, eps={w.eps}, min_pts={w.min_pts}",
-            "points": w.n, "dims": w.d, "strategy": "precomputed, threshold>=max n_k (cdist order)",
+            "points": w.n, "dims": w.d,
+            "strategy": ("precomputed, threshold>=max n_k (cdist order)" if w.threshold >= 10 ** 9
+                         else f"precomputed, threshold {w.threshold} (reference default: larger "
+                              "elements in numpy's pairwise order)"),
             "parallelism": f"cover elements sharded over {world} GPU(s)",
             "l2": "inputs (N*d*8 bytes) exceed the 126 MB L2; no flush needed"}
 
@@ -385,13 +419,17 @@ def main():
     params = workload_params(w)
     Xh = torch.from_numpy(X).pin_memory()
     Xd = Xh.to(dev)
+    # cfg4: the PCA lens is an input (FilterValues), like X
+    Fh = torch.from_numpy(workloads.pca2_lens(X)).pin_memory() if is_pca(w) else None
+    Fd = Fh.to(dev) if Fh is not None else None
     stream = torch.cuda.current_stream(dev)
 
     def step(Xdev):
         if world > 1:
-            g, st = build_distributed(Xdev, pc, params, rank, world, dist, BUDGET, args.engine)
+            g, st = build_distributed(Xdev, pc, params, rank, world, dist, BUDGET, args.engine,
+                                      F=Fd)
         else:
-            g = build_device(Xdev, pc, params, BUDGET, None, args.engine)
+            g = build_device(Xdev, pc, params, BUDGET, None, args.engine, F=Fd)
             st = g.dev_stats
         return g, st
 
@@ -453,33 +491,55 @@ def main():
     if world == 1:
         from paper_2011_03209_b200 import compute_mapper, from_array
 
-        pc_host = from_array(Xh.numpy())  # page-locked host buffer, no copy
-        run = compute_mapper(pc_host, params, engine=args.engine)
+        if Fh is None:
+            pc_host = from_array(Xh.numpy())  # page-locked host buffer, no copy
+
+            def e2e_step():
+                return compute_mapper(pc_host, params, engine=args.engine).graph
+            e2e_api = "compute_mapper -> MapperRun (graph + canonical JSON bytes)"
+        else:
+            h2d += Fh.numpy().nbytes
+
+            def e2e_step():
+                return library_pieces(Xh.numpy(), Fh.numpy(), w, params)
+            e2e_api = ("build_cover -> membership -> cluster_all -> build_graph -> graph_to_json "
+                       "(the lens is FilterValues: test_nerve.py:23-30's composition), fresh "
+                       "PointCloud/FilterValues objects every step (no device cache)")
+        gr = e2e_step()
         barrier()
         f0.record(stream)
         for _ in range(args.steps):
-            run = compute_mapper(pc_host, params, engine=args.engine)
+            gr = e2e_step()
         f1.record(stream)
         barrier()
-        gr = run.graph
         n_rows = sum(len(nd.rows) for nd in gr.nodes)
         d2h = 8 * (n_rows + gr.n_nodes + 1 + gr.n_nodes * (w.d + len(params.filters)) +
                    3 * len(gr.edges))
-        e2e_api = "compute_mapper -> MapperRun (graph + canonical JSON bytes)"
     else:
-        Xs = torch.empty_like(Xd)  # the step's input buffer (refilled from host every step)
+        # compute_mapper as one rank of the NCCL group: 1/N of X's rows H2D per
+        # rank + all-gather over NVLink, sharded build, rank 0
+        # returns the MapperRun with the canonical graph JSON
+        from paper_2011_03209_b200 import from_array
+        from paper_2011_03209_b200.pipeline import compute_mapper_spmd
+
+        pc_host = from_array(Xh.numpy())
+        # h2d stays X.nbytes: the ranks together copy X once per step
+        run = compute_mapper_spmd(pc_host, params, rank, world, dist, dev, BUDGET, None,
+                                  args.engine, Xh=Xh)
         barrier()
         f0.record(stream)
         for _ in range(args.steps):
-            Xs.copy_(Xh, non_blocking=True)
-            g2, _ = step(Xs)
-            if g2 is not None:
-                nr = g2.node_rows.cpu()
-                no = g2.node_off.cpu()
-                d2h = nr.numel() * 8 + no.numel() * 8 + g2.edges.nbytes
+            run = compute_mapper_spmd(pc_host, params, rank, world, dist, dev, BUDGET, None,
+                                      args.engine, Xh=Xh)
         f1.record(stream)
         barrier()
-        e2e_api = "build_distributed -> node rows + edges on rank 0"
+        if run is not None:
+            gr = run.graph
+            n_rows = sum(len(nd.rows) for nd in gr.nodes)
+            d2h = 8 * (n_rows + gr.n_nodes + 1 + gr.n_nodes * (w.d + len(params.filters)) +
+                       3 * len(gr.edges))
+        e2e_api = ("compute_mapper_spmd (one rank per GPU, NCCL): 1/N of X per rank H2D + "
+                   "all-gather, sharded build, MapperRun with canonical JSON on rank 0")
     t_e2e = max_over_ranks(f0.elapsed_time(f1) / 1e3)
     # collectives every rank joins before rank 0 alone reports
     pairs_all = sum_over_ranks(pairs_eval)

@@ -147,6 +147,15 @@ int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
                         const uint8_t* h_order, int engine, int32_t* d_labels,
                         int32_t* h_n_clusters, int64_t* h_stats, void* stream);
 
+/* Work estimate for scheduling elements over GPUs (clustering.py:281-315
+ * runs elements as independent tasks): per element, the number of 128 x 128
+ * tile pairs that survive the rigorous pruning bound (h_kept_tiles[k]) — the
+ * distance work the engine will do for it. Runs the grouping, gather, tile
+ * geometry and pruning of bm_cluster_elements (no distances). */
+int bm_element_work(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
+                    const int64_t* h_offsets, int64_t n_el, double eps,
+                    int64_t* h_kept_tiles, void* stream);
+
 /* Full n_rows x n_rows distance matrix of X[rows] in one exact order
  * (clustering.py:96-113 pairwise_distances for BM_ORDER_SEQUENTIAL; the
  * on-the-fly rows of clustering.py:137-139 for BM_ORDER_PAIRWISE).
@@ -182,6 +191,10 @@ int bm_big_components(void* handle, int32_t I0, int32_t I1, int32_t* d_par, int3
 int bm_big_labels(void* handle, int32_t* d_par, const int32_t* d_bmin, int32_t* d_labels,
                   int32_t* h_n_clusters);
 int bm_big_stats(void* handle, int64_t* h_stats);
+/* Kept (unpruned) tile pairs before each tile row: h_row_first[I] for I in
+ * [0, T], h_row_first[T] = all kept tile pairs. Ranks cut their windows at
+ * equal KEPT work rather than equal triangle area. */
+int bm_big_row_tiles(void* handle, int64_t* h_row_first);
 int bm_big_close(void* handle);
 /* d_par := union of the forests d_par and d_other (n entries each). */
 int bm_merge_forest(int32_t* d_par, const int32_t* d_other, int64_t n, void* stream);

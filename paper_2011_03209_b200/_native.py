@@ -69,7 +69,10 @@ _SIGNATURES = {
     "bm_big_components": (ctypes.c_int, [_vp, _c_i32, _c_i32, _vp, _vp]),
     "bm_big_labels": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bm_big_stats": (ctypes.c_int, [_vp, _vp]),
+    "bm_big_row_tiles": (ctypes.c_int, [_vp, _vp]),
     "bm_big_close": (ctypes.c_int, [_vp]),
+    "bm_element_work": (ctypes.c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_i64, ctypes.c_double,
+                                       _vp, _vp]),
     "bm_merge_forest": (ctypes.c_int, [_vp, _vp, _c_i64, _vp]),
     "bm_group_nodes": (ctypes.c_int, [_vp, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bm_nerve_edges": (ctypes.c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _vp, _vp]),

@@ -197,7 +197,7 @@ def cluster_all(pc, memberships: list, params: DbscanParams, strategy: DistanceS
     """One PullbackClustering per cover element (clustering.py:238-316), on the GPU."""
     import torch
 
-    from .device import require_gpu, to_device_f64
+    from .device import cached_device_array, require_gpu
 
     if threads < 1:
         raise DataError("threads must be >= 1")
@@ -220,7 +220,7 @@ def cluster_all(pc, memberships: list, params: DbscanParams, strategy: DistanceS
     if rows_h.min() < 0 or rows_h.max() >= pc.n_rows:
         raise DataError("membership row out of range")
     dev = require_gpu()
-    X = to_device_f64(pc.points, dev)
+    X = cached_device_array(pc, pc.points, dev)
     rows_dev = torch.from_numpy(rows_h).to(dev)
     labels, ncl, st = cluster_device(X, rows_dev, offsets, params, orders, cancel_check, engine)
     fill_stats(stats_out, sizes, orders, strategy, st)
@@ -232,13 +232,13 @@ def dbscan_rows(pc, rows, params: DbscanParams, order: int = _native.ORDER_SEQUE
     """DBSCAN over one pullback set (clustering.py:151-198) in the given exact order."""
     import torch
 
-    from .device import require_gpu, to_device_f64
+    from .device import cached_device_array, require_gpu
 
     rows_h = np.asarray(rows, dtype=np.int64)
     if rows_h.size == 0:
         return PullbackClustering(element_index, [], [])
     dev = require_gpu()
-    X = to_device_f64(pc.points, dev)
+    X = cached_device_array(pc, pc.points, dev)
     offsets = np.array([0, rows_h.size], dtype=np.int64)
     labels, ncl, _ = cluster_device(X, torch.from_numpy(rows_h).to(dev), offsets, params,
                                     np.array([order], dtype=np.uint8), None, engine)
@@ -255,7 +255,7 @@ def pairwise_distances(pc, rows, budget_bytes: int | None = None,
     hot path: the DBSCAN engine never materialises distance matrices."""
     import torch
 
-    from .device import require_gpu, stream_ptr, to_device_f64
+    from .device import cached_device_array, require_gpu, stream_ptr
 
     rows = np.asarray(rows)
     if rows.size == 0:
@@ -266,7 +266,7 @@ def pairwise_distances(pc, rows, budget_bytes: int | None = None,
         raise MatrixBudgetExceeded(
             f"{rows.size}^2 distance matrix needs {need} bytes, budget {budget}")
     dev = require_gpu()
-    X = to_device_f64(pc.points, dev)
+    X = cached_device_array(pc, pc.points, dev)
     r = torch.from_numpy(rows.astype(np.int64)).to(dev)
     out = torch.empty((rows.size, rows.size), dtype=torch.float64, device=dev)
     rc = _native.load().bm_pairwise_distances(_native.ptr(X), X.shape[0], X.shape[1],

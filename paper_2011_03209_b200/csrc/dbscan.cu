@@ -2126,6 +2126,56 @@ extern "C" int bm_big_stats(void* handle, int64_t* h_stats) {
   return BM_OK;
 }
 
+extern "C" int bm_big_row_tiles(void* handle, int64_t* h_row_first) {
+  BM_REQUIRE(handle && h_row_first, "null argument");
+  const BatchCtx& bc = static_cast<BigElement*>(handle)->bc;
+  const int64_t T = bc.ntiles[0];
+  for (int64_t I = 0; I <= T; ++I)
+    h_row_first[I] = bc.row_first[bc.tbase[0] + I] - bc.row_first[bc.tbase[0]];
+  return BM_OK;
+}
+
+extern "C" int bm_element_work(const double* d_X, int64_t n, int64_t d, const int64_t* d_rows,
+                               const int64_t* h_offsets, int64_t n_el, double eps,
+                               int64_t* h_kept_tiles, void* stream_) {
+  BM_REQUIRE(n >= 0 && d >= 1 && n_el >= 0, "bad shapes");
+  BM_REQUIRE(eps > 0.0, "eps must be positive");
+  BM_REQUIRE(h_offsets && h_kept_tiles, "null host table");
+  for (int64_t k = 0; k < n_el; ++k) {
+    BM_REQUIRE(h_offsets[k + 1] >= h_offsets[k], "offsets must be non-decreasing");
+    h_kept_tiles[k] = 0;
+  }
+  if (n_el == 0 || h_offsets[n_el] == h_offsets[0]) return BM_OK;
+  BM_REQUIRE(d_X && d_rows, "null device pointer");
+  BM_REQUIRE(h_offsets[n_el] - h_offsets[0] < (1ll << 31), "too many membership entries");
+  // chunks of elements bounded by the dense tile-pair count (flag and tile
+  // lists are sized for every pair of a chunk)
+  std::vector<uint8_t> order(n_el, (uint8_t)BM_ORDER_SEQUENTIAL);
+  int64_t k0 = 0;
+  while (k0 < n_el) {
+    int64_t k1 = k0, pairs = 0;
+    while (k1 < n_el) {
+      const int64_t T = ceil_div(h_offsets[k1 + 1] - h_offsets[k1], kTile);
+      if (k1 > k0 && pairs + T * (T + 1) / 2 > (1ll << 27)) break;
+      pairs += T * (T + 1) / 2;
+      ++k1;
+    }
+    BatchCtx bc;
+    bc.stream = (cudaStream_t)stream_;
+    bc.d = d;
+    bc.eps = eps;
+    bc.min_pts = 1;
+    bc.use_tc = false;  // geometry from the gathered rows; no quantisation
+    int64_t st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    BM_TRY(bc.setup(d_X, d_rows, h_offsets, order.data(), k0, k1, st));
+    if (bc.n_entries > 0)
+      for (int64_t i = 0; i < bc.nb_el; ++i)
+        h_kept_tiles[k0 + i] = bc.row_first[bc.tbase[i + 1]] - bc.row_first[bc.tbase[i]];
+    k0 = k1;
+  }
+  return BM_OK;
+}
+
 extern "C" int bm_big_close(void* handle) {
   if (handle) {
     BigElement* be = static_cast<BigElement*>(handle);

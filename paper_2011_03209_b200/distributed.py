@@ -28,19 +28,53 @@ import heapq
 import numpy as np
 
 
-def lpt_partition(sizes, world: int) -> list:
-    """Element ids per rank, largest n_k^2 first onto the least-loaded rank."""
+def lpt_partition(sizes, world: int, costs=None) -> list:
+    """Element ids per rank, largest cost first onto the least-loaded rank
+    (cost: `costs` if given, else n_k^2); empty elements are skipped."""
+    cost = [float(c) for c in costs] if costs is not None else [float(s) ** 2 for s in sizes]
     loads = [(0.0, r) for r in range(world)]
     heapq.heapify(loads)
     parts = [[] for _ in range(world)]
-    order = sorted(range(len(sizes)), key=lambda k: (-int(sizes[k]) ** 2, k))
+    order = sorted(range(len(sizes)), key=lambda k: (-cost[k], k))
     for k in order:
         if int(sizes[k]) == 0:
             continue
         load, r = heapq.heappop(loads)
         parts[r].append(k)
-        heapq.heappush(loads, (load + float(sizes[k]) ** 2, r))
+        heapq.heappush(loads, (load + cost[k], r))
     return [sorted(p) for p in parts]
+
+
+# Cost model for scheduling (measured at cfg3 on one B200): a kept 128 x 128
+# tile pair costs ~16 ns of distance work; the per-row stages (grouping,
+# quantisation, components, relabel) ~0.7 us per 128-row tile, i.e. ~45 kept
+# tile pairs' worth.
+ROW_TILE_COST = 45
+
+
+def element_costs(X, rows, offsets, sizes, eps, rank: int, world: int, dist) -> np.ndarray:
+    """Per-element scheduling cost: kept (unpruned) tile pairs, from the
+    engine's own pruning (bm_element_work), plus ROW_TILE_COST per row tile.
+    Each rank estimates a 1/world share of the elements (round-robin by size)
+    and one all_reduce(sum) gives every rank every estimate."""
+    import torch
+
+    from . import engine as eng
+
+    n_el = len(sizes)
+    order = sorted(range(n_el), key=lambda k: (-int(sizes[k]), k))
+    mine = sorted(k for i, k in enumerate(order) if i % world == rank and sizes[k] > 0)
+    est = torch.zeros(max(n_el, 1), dtype=torch.int64, device=X.device)
+    if mine:
+        ranges, loc = pack_local(offsets, mine)
+        rows_loc = torch.cat([rows[a:b] for a, b in ranges])
+        kept = eng.element_work(X, rows_loc, loc, eps)
+        est[torch.as_tensor(mine, device=X.device)] = torch.from_numpy(kept).to(X.device)
+    if world > 1:
+        dist.all_reduce(est, op=dist.ReduceOp.SUM)
+    kept = est.cpu().numpy()[:n_el]
+    tiles = -(-np.asarray(sizes, dtype=np.int64) // 128)
+    return kept + ROW_TILE_COST * tiles
 
 
 def pack_local(offsets: np.ndarray, elems: list) -> tuple:
@@ -56,8 +90,9 @@ def gather_labels(labels_local, ncl_local, elems: list, parts: list, offsets: np
     """All ranks contribute their elements' labels; rank 0 returns the full
     per-entry label array and per-element cluster counts (others: None).
 
-    Collective: one all_gather of a fixed-size int32 buffer per rank (labels
-    padded to the largest rank, cluster counts appended)."""
+    Collective: one gather to rank 0 of a fixed-size int32 buffer per rank
+    (labels padded to the largest rank, cluster counts appended); only rank 0
+    builds nodes and edges, so no other rank receives anything."""
     import torch
 
     sizes = [int(sum(int(offsets[k + 1] - offsets[k]) for k in p)) for p in parts]
@@ -69,13 +104,7 @@ def gather_labels(labels_local, ncl_local, elems: list, parts: list, offsets: np
     if elems:
         buf[n_loc:n_loc + len(elems)] = torch.as_tensor(np.asarray(ncl_local, dtype=np.int32),
                                                        device=device)
-    out = torch.empty((world, cap), dtype=torch.int32, device=device)
-    if dist.get_backend() == "nccl":
-        dist.all_gather_into_tensor(out, buf)
-    else:  # gloo (CPU tests of the host logic)
-        chunks = list(out.unbind(0))
-        dist.all_gather(chunks, buf)
-        out = torch.stack(chunks)
+    out = _gather_to_root(buf, rank, world, dist)
     if rank != 0:
         return None, None
     total = int(offsets[-1])
@@ -131,25 +160,57 @@ def split_window(I0: int, I1: int, T: int, max_tiles: int) -> list:
     return out
 
 
-def big_elements(sizes, world: int) -> list:
-    """Elements whose pair work exceeds 1/world of the total: row-blocked."""
+def big_elements(sizes, world: int, costs=None) -> list:
+    """Elements whose work (costs, else n_k^2) exceeds 1/world of the total:
+    row-blocked."""
     if world <= 1:
         return []
-    work = [float(s) ** 2 for s in sizes]
+    work = [float(c) for c in costs] if costs is not None else [float(s) ** 2 for s in sizes]
     total = sum(work)
     return [k for k, w in enumerate(work) if total > 0 and w > total / world]
 
 
-def _all_gather(t, world: int, dist):
+def kept_windows(row_first, world: int) -> list:
+    """Tile-row windows [I0, I1) per rank with (nearly) equal KEPT tile pairs;
+    row_first[I] = kept pairs before tile row I (T + 1 entries)."""
+    rf = np.asarray(row_first, dtype=np.float64)
+    T = len(rf) - 1
+    total = rf[-1]
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        I = int(np.searchsorted(rf, target))  # first I with rf[I] >= target
+        if I > 0 and target - rf[I - 1] < rf[min(I, T)] - target:
+            I -= 1
+        cuts.append(min(max(I, cuts[-1]), T))
+    cuts.append(T)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def split_window_kept(I0: int, I1: int, row_first, max_tiles: int) -> list:
+    """Sub-windows of [I0, I1) holding at most max_tiles kept tile pairs
+    (>= 1 row each)."""
+    out = []
+    I = I0
+    while I < I1:
+        J = I + 1
+        while J < I1 and row_first[J + 1] - row_first[I] <= max_tiles:
+            J += 1
+        out.append((I, J))
+        I = J
+    return out
+
+
+def _gather_to_root(t, rank: int, world: int, dist):
+    """(world, *t.shape) on rank 0 (None elsewhere): one gather collective."""
     import torch
 
-    if dist.get_backend() == "nccl":
-        out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t)
-        return out
-    chunks = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(chunks, t)
-    return torch.stack(chunks)
+    if world == 1:
+        return t.unsqueeze(0)
+    out = (torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+           if rank == 0 else None)
+    dist.gather(t, list(out.unbind(0)) if rank == 0 else None, dst=0)
+    return out
 
 
 def rowblock_cluster(be, rank: int, world: int, dist, max_tiles: int, merge_forest):
@@ -161,8 +222,13 @@ def rowblock_cluster(be, rank: int, world: int, dist, max_tiles: int, merge_fore
     all_reduce(min) of border minima -> labels on rank 0. Returns
     (labels, n_clusters) on rank 0, (None, None) elsewhere. The result is the
     element's unique DBSCAN labelling, identical for every world size."""
-    I0, I1 = area_windows(be.tiles, world)[rank]
-    wins = split_window(I0, I1, be.tiles, max_tiles) if I1 > I0 else []
+    if hasattr(be, "row_tiles"):  # balanced on the kept (unpruned) tile pairs
+        rf = be.row_tiles()
+        I0, I1 = kept_windows(rf, world)[rank]
+        wins = split_window_kept(I0, I1, rf, max_tiles) if I1 > I0 else []
+    else:
+        I0, I1 = area_windows(be.tiles, world)[rank]
+        wins = split_window(I0, I1, be.tiles, max_tiles) if I1 > I0 else []
     cnt = be.zeros()
     for w in wins:
         be.counts(w[0], w[1], cnt)
@@ -172,7 +238,7 @@ def rowblock_cluster(be, rank: int, world: int, dist, max_tiles: int, merge_fore
     for w in reversed(wins):  # the last window's bits are still resident
         be.components(w[0], w[1], par, bmin)
     dist.all_reduce(bmin, op=dist.ReduceOp.MIN)
-    forests = _all_gather(par, world, dist)
+    forests = _gather_to_root(par, rank, world, dist)
     if rank != 0:
         return None, None
     for r in range(1, world):
@@ -195,8 +261,12 @@ def device_window_tiles(device, d: int, rows: int) -> int:
 
 
 def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=None,
-                      engine: int = 0):
-    """Sharded hot path. Returns a DeviceGraph on rank 0 and None elsewhere."""
+                      engine: int = 0, cancel_check=None, balance: str = "kept", F=None):
+    """Sharded hot path. Returns (DeviceGraph, stats) on rank 0 and
+    (None, stats) elsewhere. balance="kept": elements and row-block windows
+    are balanced on the engine's kept tile pairs (element_costs); "area": on
+    n_k^2 / triangle area. cancel_check is polled by rank 0 between phases
+    (a raise there aborts the other ranks at their next collective)."""
     import torch
 
     from . import engine as eng
@@ -205,8 +275,9 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     from .filters import evaluate_device
     from .pipeline import DeviceGraph
 
-    cols = [evaluate_device(X, pc, s) for s in params.filters]
-    F = torch.stack(cols, dim=1).contiguous() if len(cols) > 1 else cols[0].reshape(-1, 1)
+    if F is None:  # else: the caller's (N, m) device lens (FilterValues)
+        cols = [evaluate_device(X, pc, s) for s in params.filters]
+        F = torch.stack(cols, dim=1).contiguous() if len(cols) > 1 else cols[0].reshape(-1, 1)
     rng = torch.stack([F.amin(dim=0), F.amax(dim=0)], dim=1).cpu().numpy()
     cover = build_cover_from_range([(rng[a, 0], rng[a, 1]) for a in range(F.shape[1])],
                                    params.n, params.p)
@@ -214,8 +285,12 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     sizes = np.diff(offsets)
     budget = effective_mem_budget() if budget_bytes is None else budget_bytes
     orders = element_orders(sizes, params.strategy, budget)
-    big = big_elements(sizes, world)
-    parts = lpt_partition([0 if k in big else s for k, s in enumerate(sizes)], world)
+    if rank == 0 and cancel_check is not None:
+        cancel_check()
+    costs = (element_costs(X, rows, offsets, sizes, params.eps, rank, world, dist)
+             if balance == "kept" else np.asarray(sizes, dtype=np.float64) ** 2)
+    big = big_elements(sizes, world, costs)
+    parts = lpt_partition([0 if k in big else s for k, s in enumerate(sizes)], world, costs)
     mine = parts[rank]
     ranges, loc = pack_local(offsets, mine)
     st = np.zeros(8, dtype=np.int64)
@@ -227,6 +302,8 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     else:
         labels_loc = torch.empty(0, dtype=torch.int32, device=X.device)
         ncl_loc = np.zeros(len(mine), dtype=np.int32)
+    if rank == 0 and cancel_check is not None:
+        cancel_check()
     labels, ncl = gather_labels(labels_loc, ncl_loc, mine, parts, offsets, len(sizes), rank,
                                 world, dist, X.device)
     for k in big:  # every rank takes an equal tile area of each big element

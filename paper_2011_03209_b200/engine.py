@@ -122,6 +122,19 @@ def cluster(X: torch.Tensor, rows: torch.Tensor, offsets: np.ndarray, eps: float
     return labels[: int(offsets[-1])], ncl[:n_el], stats
 
 
+def element_work(X: torch.Tensor, rows: torch.Tensor, offsets: np.ndarray, eps: float):
+    """Kept (unpruned) tile pairs per element: the distance work the engine
+    will do (bm_element_work); host int64[n_el]."""
+    n, d = X.shape
+    n_el = len(offsets) - 1
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = np.zeros(max(n_el, 1), dtype=np.int64)
+    rc = _native.load().bm_element_work(P(X), n, d, P(rows), P(offsets), n_el,
+                                        ctypes.c_double(float(eps)), P(out), stream_ptr(X.device))
+    _native.check(rc, "element work")
+    return out[:n_el]
+
+
 class BigElement:
     """Row-block protocol handle for ONE cover element sharded over ranks
     (include/b200map.h bm_big_*). Arrays cnt/par/bmin hold
@@ -163,6 +176,12 @@ class BigElement:
         _native.check(self._lib.bm_big_labels(self._h, P(par), P(bmin), P(out), P(ncl)),
                       "big labels")
         return out[: self.n_rows], int(ncl[0])
+
+    def row_tiles(self) -> np.ndarray:
+        """Kept tile pairs before each tile row (tiles + 1 entries)."""
+        out = np.zeros(self.tiles + 1, dtype=np.int64)
+        _native.check(self._lib.bm_big_row_tiles(self._h, P(out)), "big row tiles")
+        return out
 
     def stats(self) -> np.ndarray:
         st = np.zeros(8, dtype=np.int64)

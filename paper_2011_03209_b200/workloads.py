@@ -25,6 +25,7 @@ class Workload:
     overlaps: tuple
     eps: float
     min_pts: int = 5
+    threshold: int = 10 ** 9  # DistanceStrategy threshold (>= max n_k: every element cdist order)
 
 
 CONFIGS = {
@@ -33,7 +34,22 @@ CONFIGS = {
     "cfg3": Workload("cfg3", 1_000_000, 256, 10, 5.0, 3, (("l2-norm", None),), (40,), (0.3,), 21.3),
     "cfg4": Workload("cfg4", 500_000, 128, 10, 5.0, 4, ("pca2",), (15, 15), (0.3, 0.3), 14.7),
     "cfg5": Workload("cfg5", 4_000_000, 256, 10, 5.0, 5, (("l2-norm", None),), (10,), (0.3,), 21.3),
+    # cfg3-shaped at the reference's DEFAULT strategy (threshold 20,000): 5
+    # elements of 20-22k rows take numpy's pairwise (on-the-fly) order
+    # (tests/golden/cases.py cfg3_default; golden made by nervemap itself)
+    "cfg3d": Workload("cfg3d", 200_000, 256, 10, 5.0, 6, (("l2-norm", None),), (40,), (0.3,),
+                      21.3, threshold=20_000),
 }
+
+
+def pca2_lens(X: np.ndarray) -> np.ndarray:
+    """cfg4's lens: the top-2 principal-component projection (the reference's
+    analysis.pca, analysis.py:225-256, is not a FilterSpec kind, so the lens
+    is computed on the host and passed as FilterValues to both sides; SVD of
+    the centred first 20,000 rows)."""
+    Xc = X - X.mean(axis=0)
+    _, _, vt = np.linalg.svd(Xc[:20000], full_matrices=False)
+    return np.ascontiguousarray(Xc @ vt[:2].T)
 
 
 def generate(n: int, d: int, k: int, box: float, seed: int, sigma: float = 1.0) -> np.ndarray:

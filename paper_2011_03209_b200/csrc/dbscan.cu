@@ -30,16 +30,20 @@ namespace bm {
 
 bool tc_supported(int64_t d);
 struct TcPrep;
-int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
+int tc_prepare(const RowSrc src, int64_t d, const ElemTables& et, int64_t P, double eps,
                const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
                double* cen, double* rad, const double* tminmax);
 void tc_release(TcPrep* tp);
-int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
+int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
               int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
               bool sync_check, int64_t* stats, cudaStream_t stream);
 void tc_set_queue_scale(TcPrep* tp, double s);
 int tc_collect(TcPrep* tp, int64_t* rechecked, bool* overflow, cudaStream_t stream);
+int tc_tile_project(TcPrep* tp, const ElemTables& et, const int32_t* tseed,
+                    const int8_t* seeds_q, const double* unorm, double* proj,
+                    cudaStream_t stream);
+int64_t tc_kpad(int64_t d);
 
 namespace {
 
@@ -65,9 +69,10 @@ __global__ void gather_kernel(const double* __restrict__ X, int64_t d,
   }
 }
 
-// Gather fused with the per-tile column statistics the tensor-core engine
-// needs (min, max, mean = the tile centre of the pruning bound): one CTA per
-// 128-row tile, one thread per column, rows in order.
+// Per-tile column statistics the tensor-core engine needs (min, max, mean =
+// the tile centre of the pruning bound), read from X through the membership;
+// with Xg != null the rows are also gathered. One CTA per 128-row tile, one
+// thread per column, rows in order.
 __global__ void __launch_bounds__(256)
 gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                     ElemTables et, double* __restrict__ Xg, double* __restrict__ tmin,
@@ -92,11 +97,16 @@ gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
       double v = 0.0;
       if (r < valid) {
         v = X[src[r] * d + c];
-        mn = fmin(mn, v);
-        mx = fmax(mx, v);
+        // the quantisation grid spans the FINITE values: a non-finite row
+        // then only poisons its own tile's error bound (rechecked), not the
+        // element's scale
+        if (isfinite(v)) {
+          mn = fmin(mn, v);
+          mx = fmax(mx, v);
+        }
         sm += v;
       }
-      Xg[(p0 + r) * d + c] = v;
+      if (Xg) Xg[(p0 + r) * d + c] = v;
     }
     tmin[tile * d + c] = mn;
     tmax[tile * d + c] = mx;
@@ -258,7 +268,8 @@ __global__ void group_identity_kernel(const int64_t* __restrict__ offs, int64_t 
 // sorted entries -> ent (per padded row) and inv (per entry)
 __global__ void perm_kernel(const int64_t* __restrict__ sorted, const int64_t* __restrict__ offs,
                             ElemTables et, int64_t P, int32_t* __restrict__ ent,
-                            int32_t* __restrict__ inv) {
+                            int32_t* __restrict__ inv, const int64_t* __restrict__ rows,
+                            int64_t* __restrict__ xrow) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = 0, b = et.n_el;
@@ -271,8 +282,10 @@ __global__ void perm_kernel(const int64_t* __restrict__ sorted, const int64_t* _
       const int e = (int)sorted[offs[a] + i];
       ent[p] = e;
       inv[e] = (int32_t)p;
+      if (xrow) xrow[p] = rows[e];
     } else {
       ent[p] = -1;
+      if (xrow) xrow[p] = -1;
     }
   }
 }
@@ -346,6 +359,68 @@ seed_data_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restr
       sdist[((int64_t)k * kGroupSeeds + ga) * kGroupSeeds + gb] = sqrt(acc);
       if (gb == 0) snorm[(int64_t)k * kGroupSeeds + ga] = sqrt(na);
     }
+  }
+}
+
+// int8 seeds of the tensor-core direction bound (tc_engine.cu
+// tile_project_i8_kernel): per grouped element (one CTA),
+//   s'_g = clamp(rint((s_g - m) / sigma), +-127),  m = mean of the seeds,
+//   sigma = max_{g,c} |s_g,c - m_c| / 127,
+// zero-padded to kpad bytes, and |s'_a - s'_b| (exact integer sum of squares,
+// square root rounded up). Any integer direction gives a valid bound; this
+// one follows the seed differences to ~1% in 256 dimensions.
+__global__ void __launch_bounds__(256)
+seed_quant_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                  const int64_t* __restrict__ offs, const int32_t* __restrict__ elems,
+                  int64_t kpad, int8_t* __restrict__ seeds_q, double* __restrict__ unorm) {
+  const int k = elems[blockIdx.x];
+  const int64_t ek = offs[k], nk = offs[k + 1] - ek;
+  const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
+  __shared__ int64_t srow[kGroupSeeds];
+  __shared__ double smean[256];
+  __shared__ double sdev[8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t < kGroupSeeds) srow[t] = t < S ? rows[ek + (t * nk) / S] : -1;
+  __syncthreads();
+  double dev = 0.0;
+  for (int64_t c = t; c < d; c += blockDim.x) {
+    double m = 0.0;
+    for (int g = 0; g < S; ++g) m += X[srow[g] * d + c];
+    m /= (double)S;
+    smean[c] = m;
+    for (int g = 0; g < S; ++g) dev = fmax(dev, fabs(X[srow[g] * d + c] - m));
+  }
+  for (int o = 16; o; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if (lane == 0) sdev[w] = dev;
+  __syncthreads();
+  double dmax = 0.0;
+  for (int i = 0; i < 8; ++i) dmax = fmax(dmax, sdev[i]);
+  const double sigma = (dmax > 0.0 && dmax < 1e300) ? dmax / 127.0 : 1.0;
+  int8_t* sq = seeds_q + (int64_t)k * kGroupSeeds * kpad;
+  constexpr int kSS = 256 + 4;  // smem row (bytes): 65 words, conflict-free columns
+  __shared__ __align__(16) int8_t ssq[kGroupSeeds * kSS];
+  for (int64_t i = t; i < (int64_t)kGroupSeeds * kpad; i += blockDim.x) {
+    const int g = (int)(i / kpad);
+    const int64_t c = i % kpad;
+    double v = 0.0;
+    if (g < S && c < d) v = fmin(fmax(rint((X[srow[g] * d + c] - smean[c]) / sigma), -127.0), 127.0);
+    const int8_t q = (int8_t)(v == v ? (int)v : 0);
+    sq[i] = q;
+    ssq[g * kSS + c] = q;
+  }
+  __syncthreads();
+  // |s'_a - s'_b|^2 = |a|^2 + |b|^2 - 2 a.b, exact in int32 (dp4a over words)
+  for (int pr = t; pr < kGroupSeeds * kGroupSeeds; pr += blockDim.x) {
+    const int ga = pr / kGroupSeeds, gb = pr % kGroupSeeds;
+    int dot = 0, na = 0, nb = 0;
+    for (int64_t c = 0; c < kpad; c += 4) {
+      const int wa = *reinterpret_cast<const int*>(ssq + ga * kSS + c);
+      const int wb = *reinterpret_cast<const int*>(ssq + gb * kSS + c);
+      dot = __dp4a(wa, wb, dot);
+      na = __dp4a(wa, wa, na);
+      nb = __dp4a(wb, wb, nb);
+    }
+    unorm[((int64_t)k * kGroupSeeds + ga) * kGroupSeeds + gb] = __dsqrt_ru((double)(na + nb - 2 * dot));
   }
 }
 
@@ -596,7 +671,8 @@ tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
           const int sa = tseed[tb + I], sb = tseed[tb + J];
           if (sa >= 0 && sb >= 0 && sa != sb) {
             const double u = sdist[((int64_t)k * kGroupSeeds + sa) * kGroupSeeds + sb];
-            const double num = proj[(tb + I) * kGroupSeeds + sb] + proj[(tb + J) * kGroupSeeds + sa];
+            const double num =
+                __dadd_rd(proj[(tb + I) * kGroupSeeds + sb], proj[(tb + J) * kGroupSeeds + sa]);
             if (u > 0.0 && num > 0.0 && (num / (u * (1.0 + 1e-12))) * (1.0 - gamma) > eps) keep = 0;
           }
         }
@@ -1375,11 +1451,19 @@ struct BatchCtx {
   int32_t* tseed = nullptr;
   float* seed_f = nullptr;
   double *seed_norm = nullptr, *seed_dist = nullptr;
+  // direct: the tensor-core engine reads X through the membership (no
+  // gathered fp64 copy Xg) and the direction bound runs on the limb planes
+  // with int8 seeds (seeds_q; seed_dist then holds |s'_a - s'_b|)
+  bool direct = false;
+  RowSrc src{};
+  Scratch s_seedq;
+  int8_t* seeds_q = nullptr;
   TileRef* d_tiles = nullptr;
   TileUnit *d_diag = nullptr, *d_off = nullptr, *d_tcu = nullptr;
   ElemTables et{};
   int32_t *cnt = nullptr, *par = nullptr, *bmin = nullptr, *lab = nullptr, *cmin = nullptr,
           *head = nullptr, *ent = nullptr, *inv = nullptr;
+  int64_t* xrow = nullptr;  // padded index -> dataset row (-1: pad)
   int64_t* hscan = nullptr;
   uint8_t* core = nullptr;
   int64_t* d_offs = nullptr;
@@ -1434,12 +1518,17 @@ struct BatchCtx {
     BM_CHECK_CUDA(cudaMemcpyAsync(d_ntiles, ntiles.data(), nb_el * 4, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), (nb_el + 1) * 4, cudaMemcpyHostToDevice, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(d_order, order.data(), nb_el, cudaMemcpyHostToDevice, stream));
-    BM_TRY(scratch_alloc(perm, (size_t)(P + n_entries) * 4, stream));
+    BM_TRY(scratch_alloc(perm, (size_t)(P + n_entries) * 4 + 16 + (size_t)P * 8, stream));
     ent = perm.as<int32_t>();
     inv = ent + P;
+    xrow = reinterpret_cast<int64_t*>(((uintptr_t)(inv + n_entries) + 15) & ~(uintptr_t)15);
     et = ElemTables{d_tp_off, d_pbase, d_nrows, d_ntiles, d_order, ent, nb_el};
     const int64_t* rows_b = d_rows + h_offsets[k0];
     const bool prune = prune_enabled(d, eps);
+    // per-row bulk copies of X rows need 16-byte row sizes (d even);
+    // B200MAP_NO_DIRECT=1 keeps the gathered copy (A/B checks)
+    const char* no_direct = getenv("B200MAP_NO_DIRECT");
+    direct = use_tc && (d % 2 == 0) && !(no_direct && no_direct[0] == '1');
 
     trace_mark("setup:tables", stream);
     // ---- row order inside each element: grouped (stable by seed) or identity
@@ -1476,14 +1565,23 @@ struct BatchCtx {
         seed_order_kernel<<<(unsigned)gel.size(), 256, 0, stream>>>(
             d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>(), d_order);
         BM_CHECK_LAUNCH();
-        // seeds for the direction bound (fp32 copy, norms, pair distances)
+        // seeds for the direction bound (fp32 copy, norms, pair distances;
+        // direct: int8 seeds and their integer difference norms)
         BM_TRY(scratch_alloc(s_seed, (size_t)nb_el * kGroupSeeds * (d * 4 + 8 + kGroupSeeds * 8),
                              stream));
         seed_norm = s_seed.as<double>();
         seed_dist = seed_norm + nb_el * kGroupSeeds;
         seed_f = reinterpret_cast<float*>(seed_dist + (int64_t)nb_el * kGroupSeeds * kGroupSeeds);
-        seed_data_kernel<<<(unsigned)(gel.size() * kGroupSeeds), 256, 0, stream>>>(
-            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), seed_f, seed_norm, seed_dist);
+        if (direct) {
+          const int64_t kpad = tc_kpad(d);
+          BM_TRY(scratch_alloc(s_seedq, (size_t)nb_el * kGroupSeeds * kpad, stream));
+          seeds_q = s_seedq.as<int8_t>();
+          seed_quant_kernel<<<(unsigned)gel.size(), 256, 0, stream>>>(
+              d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), kpad, seeds_q, seed_dist);
+        } else {
+          seed_data_kernel<<<(unsigned)(gel.size() * kGroupSeeds), 256, 0, stream>>>(
+              d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), seed_f, seed_norm, seed_dist);
+        }
         BM_CHECK_LAUNCH();
         BM_TRY(scratch_alloc(s_it, items.size() * sizeof(GroupItem), stream));
         BM_CHECK_CUDA(cudaMemcpyAsync(s_it.ptr, items.data(), items.size() * sizeof(GroupItem),
@@ -1502,13 +1600,14 @@ struct BatchCtx {
         BM_CHECK_LAUNCH();
       }
       perm_kernel<<<grid_for(P, 256), 256, 0, stream>>>(s_v.as<int64_t>(), d_offs, et, P, ent,
-                                                        inv);
+                                                        inv, rows_b, xrow);
       BM_CHECK_LAUNCH();
     }
 
     trace_mark("setup:grouped", stream);
-    // ---- gather rows (fp64, padded order)
-    BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
+    // ---- gather rows (fp64, padded order) — the exact engine only
+    if (!direct) BM_TRY(scratch_alloc(xg, (size_t)P * d * sizeof(double), stream));
+    src = direct ? RowSrc{d_X, xrow} : RowSrc{xg.as<double>(), nullptr};
     // tile centres / radii for the pruning bound; with the tensor-core engine
     // the centres (and the column ranges of the quantisation) come out of the
     // gather itself, the radii out of the quantisation pass
@@ -1519,13 +1618,14 @@ struct BatchCtx {
     if (use_tc && prune) {
       BM_TRY(scratch_alloc(s_mm, (size_t)n_rt * d * 16, stream));
       gather_tiles_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
-          d_X, d, rows_b, et, xg.as<double>(), s_mm.as<double>(), s_mm.as<double>() + n_rt * d,
-          cen);
-    } else {
+          d_X, d, rows_b, et, direct ? nullptr : xg.as<double>(), s_mm.as<double>(),
+          s_mm.as<double>() + n_rt * d, cen);
+      BM_CHECK_LAUNCH();
+    } else if (!direct) {
       gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
                                                             xg.as<double>());
+      BM_CHECK_LAUNCH();
     }
-    BM_CHECK_LAUNCH();
 
     // ---- per-row work arrays (counts accumulate over the adjacency windows)
     const size_t wbytes = (size_t)P * (4 + 1 + 4 + 4 + 4 + 4 + 4) + (size_t)(P + 1) * 8 + 64;
@@ -1543,7 +1643,7 @@ struct BatchCtx {
     trace_mark("setup:gathered", stream);
     if (use_tc) {
       const double* tmm = s_mm.ptr ? s_mm.as<double>() : nullptr;
-      BM_TRY(tc_prepare(xg.as<double>(), d, et, P, eps, nrows, stream, &tc, cen, rad, tmm));
+      BM_TRY(tc_prepare(src, d, et, P, eps, nrows, stream, &tc, cen, rad, tmm));
       tc_set_queue_scale(tc, qscale);
     }
 
@@ -1590,9 +1690,13 @@ struct BatchCtx {
       if (tseed) {
         BM_TRY(scratch_alloc(s_proj, (size_t)n_rt * kGroupSeeds * 8, stream));
         proj = s_proj.as<double>();
-        tile_project_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
-            xg.as<double>(), d, et, n_rt, tseed, seed_f, seed_norm, cen, rad, proj);
-        BM_CHECK_LAUNCH();
+        if (direct) {
+          BM_TRY(tc_tile_project(tc, et, tseed, seeds_q, seed_dist, proj, stream));
+        } else {
+          tile_project_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
+              xg.as<double>(), d, et, n_rt, tseed, seed_f, seed_norm, cen, rad, proj);
+          BM_CHECK_LAUNCH();
+        }
       }
       for (int64_t b0 = 0; b0 < nblk; b0 += (1ll << 30)) {
         const int64_t nb = std::min<int64_t>(1ll << 30, nblk - b0);
@@ -1696,7 +1800,7 @@ struct BatchCtx {
     if (use_tc) {
       // windows (huge elements, row blocks) check the recheck queue at once so
       // that their counts accumulate exactly once; a whole batch defers it
-      BM_TRY(tc_window(tc, xg.as<double>(), et, w.tiles, w.slot0, w.n_tiles, w.tcu, w.n_tc,
+      BM_TRY(tc_window(tc, src, et, w.tiles, w.slot0, w.n_tiles, w.tcu, w.n_tc,
                        w.pairs, adj, nonempty, cnt_acc, I0 >= 0, I0 >= 0, stats, stream));
     } else {
       BM_TRY(exact_build_adjacency(xg.as<double>(), d, et, w.tiles + w.slot0, w.n_tiles, eps,
@@ -1941,7 +2045,8 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       bc.eps = eps;
       bc.min_pts = min_pts;
       bc.use_tc = use_tc;
-      bc.qscale = attempt == 0 ? 1.0 : (attempt == 1 ? 8.0 : 512.0);
+      // (the last attempt holds every pair of the window)
+      bc.qscale = attempt == 0 ? 1.0 : (attempt == 1 ? 8.0 : 2000.0);
       BM_TRY(bc.setup(d_X, d_rows, h_offsets, h_order, bt.k0, bt.k1, bst));
       if (bc.n_entries == 0) {
         empty = true;

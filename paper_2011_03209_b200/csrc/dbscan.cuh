@@ -36,6 +36,19 @@ struct ElemTables {
   int64_t n_el;
 };
 
+// Where the coordinates of padded row p come from: the gathered copy Xg
+// (xrow == nullptr: Xg + p * d) or the dataset X itself (X + xrow[p] * d,
+// xrow[p] = rows[ent[p]], -1 for pads; valid p only). The tensor-core engine
+// reads X directly (no gathered copy); the exact engine reads Xg.
+struct RowSrc {
+  const double* X;
+  const int64_t* xrow;  // padded index -> dataset row (null: X is Xg)
+  __device__ __forceinline__ int64_t index(int64_t p) const { return xrow ? xrow[p] : p; }
+  __device__ __forceinline__ const double* row(int64_t p, int64_t d) const {
+    return X + index(p) * d;
+  }
+};
+
 // kept tile pair: element k, row tile I, column tile J (slot = list index)
 struct TileRef {
   int32_t k, I, J, pad;

@@ -722,7 +722,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
 // ---------------------------------------------------------------------------
 // per 128-row tile (global tile index t): column min/max over valid rows, and
 // (when cen != null) the tile centre = column means, for the pruning bound
-__global__ void tile_minmax_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+__global__ void tile_minmax_kernel(const RowSrc src, int64_t d, ElemTables et,
                                    const int32_t* __restrict__ tile_elem, int64_t n_tiles,
                                    double* __restrict__ tmin, double* __restrict__ tmax,
                                    double* __restrict__ cen) {
@@ -734,9 +734,11 @@ __global__ void tile_minmax_kernel(const double* __restrict__ Xg, int64_t d, Ele
   for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
     double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn, sm = 0.0;
     for (int r = 0; r < valid; ++r) {
-      const double v = Xg[(p0 + r) * d + c];
-      mn = fmin(mn, v);
-      mx = fmax(mx, v);
+      const double v = src.row(p0 + r, d)[c];
+      if (isfinite(v)) {  // see gather_tiles_kernel
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+      }
       sm += v;
     }
     tmin[t * d + c] = mn;
@@ -798,8 +800,9 @@ __global__ void elem_scale_kernel(int64_t n_el, const unsigned long long* __rest
 // atomicMax per tile); with cen != null also the row's distance to its tile
 // centre -> tile radius (raw max, NaN-propagating). The block's rows stream
 // through a shared-memory ring of kQRows-row stages filled by cp.async.bulk
-// (a tile is 128 contiguous rows of Xg); the element and tile centres are
-// staged once per tile. Two rows per warp halve the per-row reduction and
+// (16 contiguous rows of Xg per stage, or — reading X through the membership
+// — one bulk copy per row, issued by the lanes of warp 0); the element and
+// tile centres are staged once per tile. Two rows per warp halve the per-row reduction and
 // bookkeeping instructions (the kernel is issue-bound, not HBM-bound).
 constexpr int kQWarps = 8;            // blockDim.x == 256
 constexpr int kQRows = 2 * kQWarps;   // rows per ring stage (one per half-warp)
@@ -808,7 +811,7 @@ constexpr int kQMaxStages = 4;
 constexpr int kQSmem = 96 * 1024;     // ring budget (d <= 256: 2 stages of 32 KB + centres)
 
 __global__ void __launch_bounds__(256, 3)
-quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTables et, int64_t P,
+quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_t P,
                 const double* __restrict__ center, const double* __restrict__ scale,
                 int8_t* __restrict__ planes, int64_t* __restrict__ nq, int32_t* __restrict__ cq,
                 unsigned long long* __restrict__ tile_e, const double* __restrict__ cen,
@@ -824,18 +827,31 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
   const int64_t n_it = my_tiles * kQIters;
   const uint32_t stage_bytes = (uint32_t)(kQRows * d * 8);
   double* const s_c = q_ring + n_stages * kQRows * d;  // element centre, tile centre
-  auto issue = [&](int64_t i, int sl) {  // iteration i into ring slot sl
+  // iteration i into ring slot sl; called by all lanes of warp 0
+  auto issue = [&](int64_t i, int sl) {
     const int64_t row0 = (blockIdx.x + (i / kQIters) * gridDim.x) * kTile + (i % kQIters) * kQRows;
     uint64_t* bar = q_full + sl;
-    mbar_expect_tx(bar, stage_bytes);
-    bulk_load(q_ring + sl * kQRows * d, Xg + row0 * d, stage_bytes, bar);
+    if (!src.xrow) {
+      if (lane == 0) {
+        mbar_expect_tx(bar, stage_bytes);
+        bulk_load(q_ring + sl * kQRows * d, src.X + row0 * d, stage_bytes, bar);
+      }
+      return;
+    }
+    const int64_t xrow = lane < kQRows ? src.xrow[row0 + lane] : -1;
+    const unsigned m = __ballot_sync(0xffffffffu, xrow >= 0);
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(__popc(m) * d * 8));
+    __syncwarp();
+    if (xrow >= 0)  // pad rows are not loaded (never read: `valid` below)
+      bulk_load(q_ring + (sl * kQRows + lane) * d, src.X + xrow * d, (uint32_t)(d * 8), bar);
   };
   if (threadIdx.x == 0) {
     for (int i = 0; i < n_stages; ++i) mbar_init(q_full + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < n_stages && i < n_it; ++i) issue(i, i);
   }
   __syncthreads();
+  if (warp == 0)
+    for (int i = 0; i < n_stages && i < n_it; ++i) issue(i, i);
   int k = 0;
   double sc = 1.0, inv = 1.0;
   // per-half-warp maxima over its rows (lane hl == 0): |M|^2, |L|^2 and the
@@ -979,7 +995,7 @@ quantize_kernel(const double* __restrict__ Xg, int64_t d, int64_t kpad, ElemTabl
     }
     // every half-warp is done with this stage: refill it
     __syncthreads();
-    if (threadIdx.x == 0 && i + n_stages < n_it) {
+    if (warp == 0 && i + n_stages < n_it) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + n_stages, slot);
     }
@@ -1083,6 +1099,132 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
   }
 }
 
+// ---------------------------------------------------------------------------
+// Direction-bound projections from the limb planes (int8 mma.sync): per
+// grouped row tile I (seed a) and every seed g of its element k,
+//   proj[I][g] = s_k * min_{x in I} <q_x, u'_ag> - e_I |u'_ag|   (rounded down)
+// where u'_ag = s'_a - s'_g is the difference of the element's int8-quantised
+// seeds (dbscan.cu seed_quant_kernel) and e_I bounds |x - c_k - s_k q_x| over
+// the tile (quantize_kernel). For every direction u,
+//   <x, u> = <c_k, u> + s_k <q_x, u> + <e_x, u>,
+// so proj[I][g] + <c_k, u'_ag> <= min_x <x, u'_ag>. In tile_prune_kernel the
+// two tiles of a pair use u'_ab and u'_ba = -u'_ab, the <c_k, u'> terms
+// cancel, and (proj[I][b] + proj[J][a]) / |u'_ab| <= |x - y| for every x in
+// I, y in J. <q_x, s'_g> is exact: the H, M, L limb products accumulate in
+// int32 (|.| <= 128 * 127 * 256) and combine in int64 (2^14 H + 2^7 M + L).
+// One CTA per row tile, 8 warps x 16 rows, all 64 seeds (8 n-tiles).
+// ---------------------------------------------------------------------------
+constexpr int kPjSeeds = 64;
+
+__device__ __forceinline__ void mma_s8_16832(int (&c)[4], const uint32_t (&a)[4],
+                                             uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NKC>
+__global__ void __launch_bounds__(256, 2)
+tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables et,
+                       const int32_t* __restrict__ tile_elem, const int32_t* __restrict__ tseed,
+                       const int8_t* __restrict__ seeds_q, const double* __restrict__ unorm,
+                       const double* __restrict__ scale,
+                       const unsigned long long* __restrict__ tile_e,
+                       double* __restrict__ proj) {
+  constexpr int kpad = NKC * kKC;
+  constexpr int kS = kpad + 16;  // padded smem row: conflict-free B fragments
+  __shared__ __align__(16) int8_t sS[kPjSeeds * kS];
+  __shared__ long long red[8][kPjSeeds];
+  const int64_t rt = blockIdx.x;
+  const int a = tseed[rt];
+  if (a < 0) return;  // block-uniform: element not grouped
+  const int k = tile_elem[rt];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int8_t* sk = seeds_q + (int64_t)k * kPjSeeds * kpad;
+  for (int i = t; i < kPjSeeds * kpad / 16; i += 256) {
+    const int g = i / (kpad / 16), c = i % (kpad / 16);
+    *reinterpret_cast<int4*>(sS + g * kS + c * 16) =
+        reinterpret_cast<const int4*>(sk + (int64_t)g * kpad)[c];
+  }
+  __syncthreads();
+  const int64_t p0 = rt * kTile;
+  const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
+  const int gid = lane >> 2, tig = lane & 3;
+  const int r0 = w * 16 + gid;  // this thread's rows: r0, r0 + 8
+  int acc[3][8][4];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[l][n][j] = 0;
+  const int8_t* arow = planes + (p0 + r0) * (int64_t)kpad + tig * 4;
+#pragma unroll 2
+  for (int ks = 0; ks < kpad / 32; ++ks) {
+    uint32_t af[3][4];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const int8_t* b = arow + (int64_t)l * P * kpad + ks * 32;
+      af[l][0] = __ldg(reinterpret_cast<const uint32_t*>(b));
+      af[l][1] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad));
+      af[l][2] = __ldg(reinterpret_cast<const uint32_t*>(b + 16));
+      af[l][3] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad + 16));
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int8_t* bp = sS + (n * 8 + gid) * kS + ks * 32 + tig * 4;
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bp);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bp + 16);
+#pragma unroll
+      for (int l = 0; l < 3; ++l) mma_s8_16832(acc[l][n], af[l], b0, b1);
+    }
+  }
+  // <q_x, s'_g> of row r0 (j = 0, 1) or r0 + 8 (j = 2, 3), column n * 8 + 2 tig + (j & 1)
+#define BM_PJ_COMB(n, j)                                                        \
+  ((long long)acc[0][n][j] * (1ll << (2 * kLimb)) + (long long)acc[1][n][j] * (1 << kLimb) + \
+   (long long)acc[2][n][j])
+  // <q_x, s'_a> of my two rows, from the lane of the same row group owning column a
+  // (static register indices only: selects, no dynamically indexed arrays)
+  const int na = a >> 3, ca = a & 7;
+  const bool odd = ca & 1;
+  long long da_lo = 0, da_hi = 0;
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+    if (n == na) {
+      da_lo = odd ? BM_PJ_COMB(n, 1) : BM_PJ_COMB(n, 0);
+      da_hi = odd ? BM_PJ_COMB(n, 3) : BM_PJ_COMB(n, 2);
+    }
+  const int src_lane = (lane & ~3) | (ca >> 1);
+  da_lo = __shfl_sync(0xffffffffu, da_lo, src_lane);
+  da_hi = __shfl_sync(0xffffffffu, da_hi, src_lane);
+  constexpr long long kMax = 0x7fffffffffffffffll;
+  const bool ok_lo = r0 < valid, ok_hi = r0 + 8 < valid;
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      long long m = min(ok_lo ? da_lo - BM_PJ_COMB(n, j) : kMax,
+                        ok_hi ? da_hi - BM_PJ_COMB(n, 2 + j) : kMax);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (gid == 0) red[w][n * 8 + tig * 2 + j] = m;
+    }
+#undef BM_PJ_COMB
+  __syncthreads();
+  if (t < kPjSeeds) {
+    long long m = red[0][t];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = min(m, red[i][t]);
+    const double e = __longlong_as_double((long long)tile_e[rt]);
+    const double u = unorm[((int64_t)k * kPjSeeds + a) * kPjSeeds + t];
+    double v = __dsub_rd(__dmul_rd(scale[k], (double)m), __dmul_ru(e, u));
+    if (!(e == e) || m == kMax || !(v == v)) v = -1.0e300;  // NaN/inf rows: no bound
+    proj[rt * kPjSeeds + t] = v;
+  }
+}
+
 __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
                                            uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
                                            int32_t* __restrict__ cnt,
@@ -1110,8 +1252,8 @@ __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
 constexpr int kRcWarps = 4;
 
 template <int DEPTH>
-__global__ void __launch_bounds__(kRcWarps * 32, 6)
-    recheck_kernel(const double* __restrict__ Xg, int64_t d, ElemTables et,
+__global__ void __launch_bounds__(kRcWarps * 32, 5)
+    recheck_kernel(const RowSrc src, int64_t d, ElemTables et,
                    const int4* __restrict__ queue, const unsigned long long* __restrict__ nq_ptr,
                    unsigned long long qcap, double eps,
                    uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
@@ -1128,6 +1270,8 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
     const bool have = i < nq;
     const int4 pr = have ? queue[i] : make_int4(0, 0, 0, 0);
     const int k = pr.w;
+    // dataset rows of the lane's pair (the queue holds valid padded rows)
+    const int64_t xa = have ? src.index(pr.x) : 0, xb = have ? src.index(pr.y) : 0;
     const int np = (nq - base) < 32 ? (int)(nq - base) : 32;
     double s_seq = 0.0, res = 0.0;
     double r[8];
@@ -1145,11 +1289,11 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int p = p0 + u;
-          const int64_t ra = __shfl_sync(0xffffffffu, pr.x, p & 31);
-          const int64_t rb = __shfl_sync(0xffffffffu, pr.y, p & 31);
+          const int64_t ra = __shfl_sync(0xffffffffu, xa, p & 31);
+          const int64_t rb = __shfl_sync(0xffffffffu, xb, p & 31);
           const bool ok = cv && p < np;
-          va[u] = ok ? __ldg(Xg + ra * d + c0 + lane) : 0.0;
-          vb[u] = ok ? __ldg(Xg + rb * d + c0 + lane) : 0.0;
+          va[u] = ok ? __ldg(src.X + ra * d + c0 + lane) : 0.0;
+          vb[u] = ok ? __ldg(src.X + rb * d + c0 + lane) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -1330,7 +1474,7 @@ struct TcPrep {
 
 // tminmax (optional): per-tile column min [n_tiles][d] then max, and cen the
 // tile centres, already computed (by the fused gather)
-int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, double eps,
+int tc_prepare(const RowSrc src, int64_t d, const ElemTables& et, int64_t P, double eps,
                const std::vector<int32_t>& h_nrows, cudaStream_t stream, TcPrep** out,
                double* cen, double* rad, const double* tminmax) {
   *out = nullptr;
@@ -1387,7 +1531,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   trace_mark("tc:prep start", stream);
   if (!tminmax) {
     tile_minmax_kernel<<<(unsigned)n_tiles, 256, 0, stream>>>(
-        Xg, d, et, tp->d_tile_elem, n_tiles, const_cast<double*>(tmin), const_cast<double*>(tmax),
+        src, d, et, tp->d_tile_elem, n_tiles, const_cast<double*>(tmin), const_cast<double*>(tmax),
         cen);
     BM_CHECK_LAUNCH();
   }
@@ -1414,7 +1558,7 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
     const int per_sm = std::max<int>(1, std::min<int>(3, (int)((220 * 1024) / smem)));
     quantize_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * per_sm), 256, smem,
                       stream>>>(
-        Xg, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
+        src, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
         reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
         cen, reinterpret_cast<unsigned long long*>(rad), tp->s_lim.as<uint32_t>(), n_stages);
     BM_CHECK_LAUNCH();
@@ -1437,6 +1581,26 @@ int tc_prepare(const double* Xg, int64_t d, const ElemTables& et, int64_t P, dou
   tp = nullptr;  // disarm the guard
   return BM_OK;
 }
+
+int tc_tile_project(TcPrep* tp, const ElemTables& et, const int32_t* tseed,
+                    const int8_t* seeds_q, const double* unorm, double* proj,
+                    cudaStream_t stream) {
+  const double* scale = tp->s_cs.as<double>() + tp->n_el * tp->d;
+  const unsigned grid = (unsigned)tp->n_tiles;
+  if (grid == 0) return BM_OK;
+  if (tp->nkc == 1)
+    tile_project_i8_kernel<1><<<grid, 256, 0, stream>>>(
+        tp->s_pl.as<int8_t>(), tp->P, et, tp->d_tile_elem, tseed, seeds_q, unorm, scale,
+        tp->s_te.as<unsigned long long>(), proj);
+  else
+    tile_project_i8_kernel<2><<<grid, 256, 0, stream>>>(
+        tp->s_pl.as<int8_t>(), tp->P, et, tp->d_tile_elem, tseed, seeds_q, unorm, scale,
+        tp->s_te.as<unsigned long long>(), proj);
+  BM_CHECK_LAUNCH();
+  return BM_OK;
+}
+
+int64_t tc_kpad(int64_t d) { return ceil_div(d, kKC) * kKC; }
 
 void tc_release(TcPrep* tp) { delete tp; }
 
@@ -1478,7 +1642,7 @@ __global__ void add_counts_kernel(int32_t* __restrict__ dst, const int32_t* __re
 // sync_check: synchronise after the MMA pass and retry it with a larger queue
 // on overflow (counts are accumulated exactly once); otherwise nothing
 // synchronises and an overflow is reported by tc_collect.
-int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef* tiles,
+int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef* tiles,
               int64_t slot0, int64_t n_tiles, const TileUnit* units, int64_t n_units,
               int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
               bool sync_check, int64_t* stats, cudaStream_t stream) {
@@ -1597,17 +1761,17 @@ int tc_window(TcPrep* tp, const double* Xg, const ElemTables& et, const TileRef*
     const int4* q = s_q.as<int4>();
     switch (tp->depth) {
       case 1:
-        recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+        recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
                                                             adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;
       case 2:
-        recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+        recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
                                                             adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;
       default:
-        recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(Xg, d, et, q, d_cnt, qcap, tp->eps,
+        recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
                                                             adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;

@@ -139,3 +139,21 @@ print("rechecks", st[1])
                            timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         assert int(r.stdout.split()[-1]) > int(qcap)  # the queue did overflow
+
+
+@pytest.mark.parametrize("d", [32, 48, 64, 200, 256])
+def test_direct_rows_equal_gathered_copy(monkeypatch, d):
+    """The tensor-core engine reading X through the membership (int8 direction
+    bound on the limb planes; default for even d) equals the engine on the
+    gathered fp64 copy (fp32 direction bound; B200MAP_NO_DIRECT=1) and the
+    oracle, with pruning on, grouped elements and NaN/inf rows."""
+    X = O.gmm(3000, d, 6, 3.0, 40 + d)
+    X[[5, 1700]] = np.nan
+    X[[42], 3] = np.inf
+    eps = O.dist_quantile(X[np.isfinite(X).all(axis=1)], 0.04, 2)
+    rows = np.arange(3000)
+    want = O.dbscan_labels(O.neighbour_matrix(X, eps, O.ORDER_SEQUENTIAL), 5)
+    lab, _, _ = labels(X, [rows], eps, 5, [O.ORDER_SEQUENTIAL], 2)
+    monkeypatch.setenv("B200MAP_NO_DIRECT", "1")
+    lab_g, _, _ = labels(X, [rows], eps, 5, [O.ORDER_SEQUENTIAL], 2)
+    assert lab.tolist() == want.tolist() == lab_g.tolist()

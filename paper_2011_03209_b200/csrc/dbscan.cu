@@ -1959,6 +1959,7 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
   if (h_offsets[n_el] == h_offsets[0]) return BM_OK;
   BM_REQUIRE(d_X && d_rows && d_labels, "null device pointer");
   BM_REQUIRE(h_offsets[n_el] - h_offsets[0] < (1ll << 31), "too many membership entries");
+  BM_REQUIRE(n < (1ll << 31), "more than 2^31 - 1 points");
   PwProgram probe;
   BM_TRY(make_pw_program(d, &probe));
 
@@ -2163,7 +2164,7 @@ extern "C" int bm_big_open(const double* d_X, int64_t n, int64_t d, const int64_
                            void* stream, void** handle, int64_t* h_tiles) {
   BM_REQUIRE(handle && h_tiles, "null output");
   *handle = nullptr;
-  BM_REQUIRE(n >= 0 && d >= 1 && n_rows >= 1, "bad shapes");
+  BM_REQUIRE(n >= 0 && n < (1ll << 31) && d >= 1 && n_rows >= 1, "bad shapes");
   BM_REQUIRE(d_X && d_rows, "null device pointer");
   BM_REQUIRE(eps > 0.0, "eps must be positive");
   BM_REQUIRE(min_pts >= 1, "min-pts must be >= 1");

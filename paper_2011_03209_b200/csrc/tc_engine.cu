@@ -1252,7 +1252,7 @@ __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
 constexpr int kRcWarps = 4;
 
 template <int DEPTH>
-__global__ void __launch_bounds__(kRcWarps * 32, 5)
+__global__ void __launch_bounds__(kRcWarps * 32, 6)
     recheck_kernel(const RowSrc src, int64_t d, ElemTables et,
                    const int4* __restrict__ queue, const unsigned long long* __restrict__ nq_ptr,
                    unsigned long long qcap, double eps,
@@ -1271,7 +1271,8 @@ __global__ void __launch_bounds__(kRcWarps * 32, 5)
     const int4 pr = have ? queue[i] : make_int4(0, 0, 0, 0);
     const int k = pr.w;
     // dataset rows of the lane's pair (the queue holds valid padded rows)
-    const int64_t xa = have ? src.index(pr.x) : 0, xb = have ? src.index(pr.y) : 0;
+    // (dataset row ids fit int32: bm_cluster_elements requires n < 2^31)
+    const int xa = have ? (int)src.index(pr.x) : 0, xb = have ? (int)src.index(pr.y) : 0;
     const int np = (nq - base) < 32 ? (int)(nq - base) : 32;
     double s_seq = 0.0, res = 0.0;
     double r[8];

@@ -237,32 +237,62 @@ class RefSampler:
         self.wall += res["wall"]
         return res["wall"]
 
+    def critical(self, target_s):
+        """Per-row rate of the largest element measured ALONE (one process,
+        no other worker contending for cores and memory): the critical path of
+        the reference's pool runs that element while most workers are idle."""
+        import time as _t
+
+        from oracle import ref_timing as RT
+
+        k = int(np.argmax(self.sizes))
+        n = int(self.sizes[k])
+        r = max(1, min(n, int(target_s / max(n * self.w.d * 1.0e-9, 1e-12))))
+        idx = np.minimum((np.arange(r) * (n / r)).astype(np.int64), n - 1)
+        RT._CTX.update(X=self.X, members=self.members, eps=self.w.eps, min_pts=self.w.min_pts,
+                       orders=self.orders)
+        t0 = _t.perf_counter()
+        _, rr, sec = RT._sample_rows(k, idx)
+        self.crit = (k, rr, sec, _t.perf_counter() - t0)
+        return sec / rr * n
+
     def estimate(self):
         from oracle import ref_timing as RT
 
         ok = self.rows > 0
         el = np.zeros(len(self.sizes))
         el[ok] = self.secs[ok] / self.rows[ok] * self.sizes[ok]
-        makespan = RT.schedule_makespan(el, self.workers)
-        wall = self.t_lens_cover + makespan
+        # per-element times measured with every worker busy (contended)
+        fifo = RT.schedule_makespan(el, self.workers)
+        k, rr, sec, _ = getattr(self, "crit", (int(np.argmax(self.sizes)), 1, 0.0, 0.0))
+        crit = sec / rr * self.sizes[k] if sec > 0 else float(el.max())
+        # lower bound of the reference's wall time (the most favourable to the
+        # reference): the largest element alone at its uncontended rate, or the
+        # contended total spread over every worker, whichever is longer
+        bound = max(crit, float(el.sum()) / self.workers)
+        wall = self.t_lens_cover + bound
         pair_dims = float((self.rows * self.sizes).sum()) * self.w.d
         frac = float((self.rows * self.sizes).sum() / max((self.sizes.astype(float) ** 2).sum(), 1))
         return {
             "value": self.w.n / wall, "unit": UNIT, "cores": self.workers, "kind": "port",
             "seconds_full_build": wall,
             "sample": (f"nervemap's CPU path (oracle/ref_timing.py: cdist rows, count_nonzero, "
-                       f"BFS neighbour queries + per-neighbour loop) on {self.workers} processes; "
-                       f"every one of the {int((self.sizes > 0).sum())} cover elements of "
-                       f"{self.w.name} sampled ({int(self.rows.max())} rows per element max, "
-                       f"{100 * frac:.3f}% of the n_k^2 pair work, {self.wall:.1f}s wall), "
-                       f"element time = measured per-row time x n_k, scheduled like "
-                       f"clustering.py:281-315 (FIFO in element order): "
-                       f"{wall:.0f}s predicted build = lens+cover {self.t_lens_cover:.1f}s "
-                       f"(measured, full size) + DBSCAN makespan {makespan:.0f}s "
-                       f"(single-worker total {el.sum():.0f}s, largest element {el.max():.0f}s); "
-                       f"nerve/payload/JSON excluded (~3 s in the reference)"),
+                       f"BFS neighbour queries + per-neighbour loop); every one of the "
+                       f"{int((self.sizes > 0).sum())} cover elements of {self.w.name} sampled on "
+                       f"{self.workers} busy processes ({int(self.rows.max())} rows per element "
+                       f"max, {100 * frac:.3f}% of the n_k^2 pair work, {self.wall:.1f}s wall; "
+                       f"element time = measured per-row time x n_k), the largest element "
+                       f"({int(self.sizes[k])} rows) also sampled alone ({rr} rows): "
+                       f"{wall:.0f}s build = lens+cover {self.t_lens_cover:.1f}s (measured, full "
+                       f"size) + max(largest element alone {crit:.0f}s, contended single-worker "
+                       f"total {el.sum():.0f}s / {self.workers} workers) — a lower bound of the "
+                       f"reference's time (its FIFO pool, clustering.py:281-315, simulated on the "
+                       f"contended times: {self.t_lens_cover + fifo:.0f}s); nerve/payload/JSON "
+                       f"excluded (~3 s in the reference)"),
             "ns_per_pair_dim": 1e9 * float(self.secs.sum()) / max(pair_dims, 1.0),
-            "single_worker_s": float(el.sum()), "critical_element_s": float(el.max()),
+            "ns_per_pair_dim_alone": 1e9 * sec / max(rr * float(self.sizes[k]) * self.w.d, 1.0),
+            "single_worker_s": float(el.sum()), "critical_element_s": float(crit),
+            "fifo_contended_s": self.t_lens_cover + fifo,
             "sampled_pair_fraction": frac,
         }
 
@@ -289,6 +319,7 @@ def cpu_baseline(X, w, target_s, workers):
                           f"(oracle/ref_timing.full_build), {r['seconds']:.1f}s measured"}
     rs = RefSampler(X, w, workers)
     rs.step(target_s, seed=0)
+    rs.critical(min(5.0, target_s))
     return {k: v for k, v in rs.estimate().items()
             if k in ("value", "unit", "cores", "kind", "sample")}
 
@@ -322,13 +353,14 @@ def run_reference(args, w, rank, world):
         t0 = _t.perf_counter()
         for i in range(steps):
             rs.step(per_step, seed=i)
+        rs.critical(min(10.0, per_step))
         est = rs.estimate()
         v = est["value"]
         ms = 1e3 * est["seconds_full_build"]
         cb = {k: est[k] for k in ("value", "unit", "cores", "kind", "sample")}
         extra["reference_model"] = {k: est[k] for k in (
-            "ns_per_pair_dim", "single_worker_s", "critical_element_s", "sampled_pair_fraction",
-            "seconds_full_build")}
+            "ns_per_pair_dim", "ns_per_pair_dim_alone", "single_worker_s", "critical_element_s",
+            "fifo_contended_s", "sampled_pair_fraction", "seconds_full_build")}
         extra["reference_model"]["sample_wall_s"] = _t.perf_counter() - t0
         # a fully measured anchor in the same run: the whole cfg2 build, and
         # the sampling model applied to cfg2 (checks the model against it)
@@ -336,6 +368,7 @@ def run_reference(args, w, rank, world):
         full2 = full_build_baseline(w2, workers)
         rs2 = RefSampler(workloads.points(w2), w2, workers)
         rs2.step(max(2.0, 0.1 * full2["cluster_s"]), seed=0)
+        rs2.critical(2.0)
         extra["measured_full_build"] = full2
         extra["measured_full_build"]["model_predicted_s"] = rs2.estimate()["seconds_full_build"]
     line = {
@@ -348,6 +381,41 @@ def run_reference(args, w, rank, world):
         **extra,
     }
     print(json.dumps(line), flush=True)
+
+
+def subsystem_roofline(w, g, st, params):
+    """HBM-bound subsystems of the last timed build (device time between the
+    build's stage events, CUDA events on the launch stream) against SURVEY
+    §8(d)'s algorithmic bytes, and the measured HBM peak."""
+    from paper_2011_03209_b200.pipeline import stage_ms
+
+    ms = stage_ms(g)
+    p, _ = peaks()
+    hbm = p.get("hbm_gbs", 6465.5)
+    n, d, m = w.n, w.d, len(params.filters)
+    entries = float(np.asarray(g.sizes).sum())
+    node_rows = float(g.node_rows.numel())
+    lens_bytes = 0.0 if is_pca(w) else float(n * d * 8 + n * 8)
+    rows = {
+        "lens": (ms.get("lens", 0.0), lens_bytes, "N*d*8 + N*8"),
+        "binning": (ms.get("cover", 0.0), n * m * 8 + entries * 8 + n * 4,
+                    "N*m*8 + sum n_k*8 + N*4 (lens range + cover + membership)"),
+        "components_border": (st[7] / 1e6, entries * (4 + 1 + 4 + 4 + 8),
+                              "sum n_k*(4+1+4+4+8) (core, union-find, border, relabel)"),
+        "nerve": (ms.get("nerve", 0.0), node_rows * (8 + 4) * 2,
+                  "node rows*(8+4)*2 (node grouping + edges)"),
+    }
+    out = {}
+    for name, (t_ms, b, how) in rows.items():
+        gbs = b / (t_ms * 1e-3) / 1e9 if t_ms > 0 else 0.0
+        out[name] = {"ms": t_ms, "alg_bytes": b, "alg_GBps": gbs, "frac_hbm": gbs / hbm,
+                     "bytes": how}
+    out["components_border"]["bitmap_bytes"] = float(st[4])
+    out["components_border"]["note"] = ("the union-find and border passes read the eps bitmap "
+                                        "(bitmap_bytes), far above the algorithmic bytes")
+    out["dbscan_prep_ms"] = st[6] / 1e6
+    out["stage_ms"] = ms
+    return out
 
 
 def library_pieces(Xnp, Fnp, w, params):
@@ -479,6 +547,7 @@ def main():
     adj_s = max_over_ranks(adj_ns / 1e9) / args.steps
     if g is not None:
         sizes = g.sizes
+    subsystems = subsystem_roofline(w, g, st, params) if world == 1 and g is not None else None
 
     # ---- end-to-end timed region: host X in (page-locked), result out.
     # One GPU: the reference-facing call itself, compute_mapper(pc, params)
@@ -586,6 +655,7 @@ def main():
                      "ceiling_frac_exact_int8": (4500.0 / 6.0) / peak,
                      "peak_source": f"{src} bf16 sustained"},
         "gpu_launches": int(launches),
+        "subsystems": subsystems,
         "nodes": int(g.n_nodes), "edges": int(len(g.edges)),
         "clocks": clk.summary(),
     }

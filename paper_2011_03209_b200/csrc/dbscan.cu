@@ -114,6 +114,53 @@ gather_tiles_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
   }
 }
 
+// The same statistics without the gather (the tensor-core engine reading X
+// directly; d even): 2 columns per thread (16-byte loads), 8 rows in flight.
+__device__ __forceinline__ void stat_acc(double v, double& mn, double& mx, double& sm) {
+  if (isfinite(v)) {  // finite grid: see gather_tiles_kernel
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  sm += v;
+}
+
+__global__ void __launch_bounds__(128)
+tile_stats_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ xrow,
+                  double* __restrict__ tmin, double* __restrict__ tmax,
+                  double* __restrict__ cen) {
+  const int64_t tile = blockIdx.x;
+  const int64_t p0 = tile * kTile;
+  __shared__ int64_t src[kTile];
+  const int64_t xr = xrow[p0 + threadIdx.x];  // blockDim.x == kTile
+  src[threadIdx.x] = xr;
+  const int valid = __syncthreads_count(xr >= 0);  // pads at the tile's end
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int64_t c = 2 * threadIdx.x; c < d; c += 2 * blockDim.x) {
+    double mn0 = inf, mx0 = -inf, sm0 = 0.0, mn1 = inf, mx1 = -inf, sm1 = 0.0;
+    int r = 0;
+    for (; r + 8 <= valid; r += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = __ldg(reinterpret_cast<const double2*>(X + src[r + u] * d + c));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        stat_acc(v[u].x, mn0, mx0, sm0);
+        stat_acc(v[u].y, mn1, mx1, sm1);
+      }
+    }
+    for (; r < valid; ++r) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(X + src[r] * d + c));
+      stat_acc(v.x, mn0, mx0, sm0);
+      stat_acc(v.y, mn1, mx1, sm1);
+    }
+    *reinterpret_cast<double2*>(tmin + tile * d + c) = make_double2(mn0, mn1);
+    *reinterpret_cast<double2*>(tmax + tile * d + c) = make_double2(mx0, mx1);
+    *reinterpret_cast<double2*>(cen + tile * d + c) =
+        make_double2(sm0 / (double)valid, sm1 / (double)valid);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Spatial grouping inside an element (performance only — any order gives the
 // same result, the order-dependent rules run on entry indices). Each entry
@@ -1037,6 +1084,14 @@ __device__ __forceinline__ uint32_t bit_transpose_step(uint32_t w, int s, uint32
   return (lane & s) ? ((w & ~m) | ((t >> s) & m)) : ((w & m) | ((t << s) & ~m));
 }
 
+#ifdef BM_COMP_STATS
+// dev counters (-DBM_COMP_STATS): tiles by path, unions, merges
+__device__ unsigned long long g_comp_stats[8];
+#define COMP_STAT(i) (threadIdx.x == 0 ? atomicAdd(&g_comp_stats[i], 1ull) : 0ull)
+#else
+#define COMP_STAT(i) 0ull
+#endif
+
 template <bool DIAG>
 __global__ void __launch_bounds__(128)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
@@ -1070,13 +1125,18 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
       const int64_t g = un.off + s;
       const int J = tiles[g].J;
       const int pJ = (int)(pb + J * kTile);
+      (void)COMP_STAT(0);
       if (!DIAG) {
-        if (!nonempty[g - slot0]) continue;  // no bit: nothing to join (block-uniform)
+        if (!nonempty[g - slot0]) {
+          (void)COMP_STAT(1);
+          continue;  // no bit: nothing to join (block-uniform)
+        }
         if (uI >= 0) {
           // both tiles all-core with one root each: the tile's bits can only
           // join the two roots (border rules need non-core rows: none here)
           const int uJ = uni[(pb >> 7) + J];
           if (uJ >= 0) {
+            (void)COMP_STAT(2);
             if (t == 0 && uI != uJ) uf_union(par, uI, uJ);
             continue;  // block-uniform
           }
@@ -1120,6 +1180,7 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         const int mnJ = min(min(rmm[2][0], rmm[2][1]), min(rmm[2][2], rmm[2][3]));
         const int mxJ = max(max(rmm[3][0], rmm[3][1]), max(rmm[3][2], rmm[3][3]));
         uniform = (mxI < 0 || mnI == mxI) && (mxJ < 0 || mnJ == mxJ);
+        (void)COMP_STAT(uniform ? 3 : 4);
         if (uniform) {
           const bool hit = ci && (((bits[r * 4] & coreJ[0]) | (bits[r * 4 + 1] & coreJ[1]) |
                                    (bits[r * 4 + 2] & coreJ[2]) | (bits[r * 4 + 3] & coreJ[3])) != 0u);
@@ -1209,6 +1270,7 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         }
       }
       __syncthreads();
+      if (any_merge) (void)COMP_STAT(5);
       // --- propagate local merges to the global forest
       if (any_merge) {
         for (int x = t; x < 2 * kTile; x += blockDim.x) {
@@ -1617,9 +1679,13 @@ struct BatchCtx {
     Scratch s_mm;
     if (use_tc && prune) {
       BM_TRY(scratch_alloc(s_mm, (size_t)n_rt * d * 16, stream));
-      gather_tiles_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
-          d_X, d, rows_b, et, direct ? nullptr : xg.as<double>(), s_mm.as<double>(),
-          s_mm.as<double>() + n_rt * d, cen);
+      if (direct)
+        tile_stats_kernel<<<(unsigned)n_rt, kTile, 0, stream>>>(
+            d_X, d, xrow, s_mm.as<double>(), s_mm.as<double>() + n_rt * d, cen);
+      else
+        gather_tiles_kernel<<<(unsigned)n_rt, 256, 0, stream>>>(
+            d_X, d, rows_b, et, xg.as<double>(), s_mm.as<double>(), s_mm.as<double>() + n_rt * d,
+            cen);
       BM_CHECK_LAUNCH();
     } else if (!direct) {
       gather_kernel<<<grid_for(P, 8, 64), 256, 0, stream>>>(d_X, d, rows_b, et, P,
@@ -1861,10 +1927,32 @@ struct BatchCtx {
       tile_uniform_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(et, n_rt, core, par_w,
                                                                      s_uni.as<int32_t>());
       BM_CHECK_LAUNCH();
+#ifdef BM_COMP_STATS
+      {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        BM_CHECK_CUDA(cudaMemcpyToSymbolAsync(g_comp_stats, z, sizeof(z), 0,
+                                              cudaMemcpyHostToDevice, stream));
+      }
+#endif
       components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
           adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w, s_uni.as<int32_t>(),
           nonempty);
       BM_CHECK_LAUNCH();
+#ifdef BM_COMP_STATS
+      {
+        unsigned long long h[8];
+        BM_CHECK_CUDA(cudaMemcpyFromSymbolAsync(h, g_comp_stats, sizeof(h), 0,
+                                                cudaMemcpyDeviceToHost, stream));
+        BM_CHECK_CUDA(cudaStreamSynchronize(stream));
+        std::vector<int32_t> hu(n_rt);
+        BM_CHECK_CUDA(cudaMemcpy(hu.data(), s_uni.ptr, n_rt * 4, cudaMemcpyDeviceToHost));
+        int64_t nu = 0;
+        for (auto v : hu) nu += v >= 0;
+        fprintf(stderr, "[comp-stats] off-diag tiles %llu: empty %llu, both-uniform %llu, "
+                "rmm-uniform %llu, full %llu, merged %llu; uniform row tiles %lld / %lld\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], (long long)nu, (long long)n_rt);
+      }
+#endif
     }
     return BM_OK;
   }

@@ -794,6 +794,140 @@ __global__ void elem_scale_kernel(int64_t n_el, const unsigned long long* __rest
   scale[k] = Rk > 0.0 ? Rk / (double)((1 << kQBits) - 2) : 1.0;
 }
 
+// Quantise one padded row (one half-warp; both half-warps of a warp call this
+// together): limbs into the three planes (4 columns per lane per pass, packed
+// 32-bit stores) and the row sums over the half-warp: N = sum q^2 (exact),
+// |M|^2, |L|^2, sum e^2 (e = x - c - s q, fp64), sum y^2, and with ct != null
+// the squared distance to the tile centre.
+struct QRow {
+  unsigned long long nsum;
+  uint32_t msq, lsq;
+  double esum, ysum, rsum;
+};
+__device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
+                                             const double* __restrict__ ck,
+                                             const double* __restrict__ ct, bool valid, int64_t d,
+                                             int64_t kpad, double sc, double inv,
+                                             int8_t* __restrict__ hrow_p,
+                                             int8_t* __restrict__ mrow_p,
+                                             int8_t* __restrict__ lrow_p, int hl, int half) {
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr double kQMax = (double)((1 << kQBits) - 1);
+  const bool vec = (d & 1) == 0;  // 16-byte aligned rows
+  uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
+  double esum = 0.0, ysum = 0.0, rsum = 0.0, nsd = 0.0;
+  // Fast path (full 4-column groups of a valid row): rint and the integer
+  // conversion by the 1.5 * 2^52 trick (exact rint, ties to even, for
+  // |v| < 2^51), byte packing with PRMT, limb norms with DP4A, sum q^2 in
+  // fp64 (per lane <= 16 * 2^42: exact). A row with any |v| >= qmax
+  // (clamping, inf, NaN) is redone by the generic path.
+  bool bad = false;
+  if (valid) {
+    for (int64_t c4 = 4 * hl; c4 < kpad && c4 + 4 <= d; c4 += 64) {
+      double xv[4], cv[4], tv[4];
+      if (vec) {
+        const double2 u0 = *reinterpret_cast<const double2*>(xr + c4);
+        const double2 u1 = *reinterpret_cast<const double2*>(xr + c4 + 2);
+        xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
+        const double2 c0 = *reinterpret_cast<const double2*>(ck + c4);
+        const double2 c1 = *reinterpret_cast<const double2*>(ck + c4 + 2);
+        cv[0] = c0.x, cv[1] = c0.y, cv[2] = c1.x, cv[3] = c1.y;
+        if (ct) {
+          const double2 t0 = *reinterpret_cast<const double2*>(ct + c4);
+          const double2 t1 = *reinterpret_cast<const double2*>(ct + c4 + 2);
+          tv[0] = t0.x, tv[1] = t0.y, tv[2] = t1.x, tv[3] = t1.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xv[j] = xr[c4 + j];
+          cv[j] = ck[c4 + j];
+          tv[j] = ct ? ct[c4 + j] : 0.0;
+        }
+      }
+      int q[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double y = xv[j] - cv[j];
+        const double v = y * inv;
+        bad |= !(fabs(v) < kQMax);
+        const double tq = __dadd_rn(v, kMagic);
+        const double qd = __dsub_rn(tq, kMagic);
+        q[j] = __double2loint(tq);
+        const double e = y - qd * sc;
+        esum += e * e;
+        ysum += y * y;
+        nsd = fma(qd, qd, nsd);
+        if (ct) {
+          const double dr = xv[j] - tv[j];
+          rsum += dr * dr;
+        }
+      }
+      const uint32_t lw = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
+                                      __byte_perm(q[2], q[3], 0x0040), 0x5410) & 0x7f7f7f7fu;
+      const uint32_t mw = __byte_perm(__byte_perm(q[0] >> kLimb, q[1] >> kLimb, 0x0040),
+                                      __byte_perm(q[2] >> kLimb, q[3] >> kLimb, 0x0040),
+                                      0x5410) & 0x7f7f7f7fu;
+      const uint32_t hw = __byte_perm(
+          __byte_perm(q[0] >> (2 * kLimb), q[1] >> (2 * kLimb), 0x0040),
+          __byte_perm(q[2] >> (2 * kLimb), q[3] >> (2 * kLimb), 0x0040), 0x5410);
+      msq = __dp4a(mw, mw, msq);
+      lsq = __dp4a(lw, lw, lsq);
+      *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
+      *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
+      *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
+    }
+  }
+  unsigned long long nsum = (unsigned long long)nsd;
+  const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
+  if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
+  // generic path: the tail columns (or the whole row when redo / padding)
+  for (int64_t c4 = 4 * hl; c4 < kpad; c4 += 64) {
+    if (!redo && valid && c4 + 4 <= d) continue;
+    uint32_t hw = 0, mw = 0, lw = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = c4 + j;
+      int q = 0;
+      if (valid && c < d) {
+        const double x = xr[c];
+        const double y = x - ck[c];
+        double qd = rint(y * inv);
+        qd = fmin(fmax(qd, -kQMax), kQMax);
+        q = (int)qd;
+        const double e = y - qd * sc;
+        esum += e * e;
+        ysum += y * y;
+        if (ct) {
+          const double dr = x - ct[c];
+          rsum += dr * dr;
+        }
+      }
+      nsum += (unsigned long long)((long long)q * q);
+      const uint32_t mq = (q >> kLimb) & ((1 << kLimb) - 1), lq = q & ((1 << kLimb) - 1);
+      msq += mq * mq;
+      lsq += lq * lq;
+      hw |= (uint32_t)(uint8_t)(int8_t)(q >> (2 * kLimb)) << (8 * j);
+      mw |= mq << (8 * j);
+      lw |= lq << (8 * j);
+    }
+    *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
+    *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
+    *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
+  }
+    // row sums over the 16 lanes of the half-warp
+#pragma unroll
+  for (int o = 8; o; o >>= 1) {
+    esum += __shfl_xor_sync(0xffffffffu, esum, o);
+    ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
+    rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+    nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+    msq += __shfl_xor_sync(0xffffffffu, msq, o);
+    lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
+  }
+  return QRow{nsum, msq, lsq, esum, ysum, rsum};
+}
+
 // One block per tile (grid-stride), one HALF-warp per padded row: limbs into
 // the three planes (4 columns per lane per pass, packed 32-bit stores),
 // N = sum q^2 (exact), e = |x - c - s q| (fp64) -> tile max (bit pattern, one
@@ -862,9 +996,6 @@ quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_
   uint32_t phase = 0;
   int64_t t = blockIdx.x;
   int sub = 0;  // row group within the tile
-  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  constexpr double kQMax = (double)((1 << kQBits) - 1);
-  const bool vec = (d & 1) == 0;  // 16-byte aligned rows in the ring
   for (int64_t i = 0; i < n_it; ++i) {
     if (sub == 0) {
       int64_t a = 0, bb = et.n_el;
@@ -889,110 +1020,12 @@ quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_
     const bool valid = (p - et.pbase[k]) < et.nrows[k];
     const double* ck = s_c;
     const double* ct = cen ? s_c + d : nullptr;
-    uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
-    double esum = 0.0, ysum = 0.0, rsum = 0.0, nsd = 0.0;
-    int8_t* const hrow_p = planes + p * kpad;
-    int8_t* const mrow_p = planes + P * kpad + p * kpad;
-    int8_t* const lrow_p = planes + 2 * P * kpad + p * kpad;
-    // Fast path (full 4-column groups of a valid row): rint and the integer
-    // conversion by the 1.5 * 2^52 trick (exact rint, ties to even, for
-    // |v| < 2^51), byte packing with PRMT, limb norms with DP4A, sum q^2 in
-    // fp64 (per lane <= 16 * 2^42: exact). A row with any |v| >= qmax
-    // (clamping, inf, NaN) is redone by the generic path.
-    bool bad = false;
-    if (valid) {
-      for (int64_t c4 = 4 * hl; c4 < kpad && c4 + 4 <= d; c4 += 64) {
-        double xv[4], cv[4], tv[4];
-        if (vec) {
-          const double2 u0 = *reinterpret_cast<const double2*>(xr + c4);
-          const double2 u1 = *reinterpret_cast<const double2*>(xr + c4 + 2);
-          xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
-          const double2 c0 = *reinterpret_cast<const double2*>(ck + c4);
-          const double2 c1 = *reinterpret_cast<const double2*>(ck + c4 + 2);
-          cv[0] = c0.x, cv[1] = c0.y, cv[2] = c1.x, cv[3] = c1.y;
-          if (ct) {
-            const double2 t0 = *reinterpret_cast<const double2*>(ct + c4);
-            const double2 t1 = *reinterpret_cast<const double2*>(ct + c4 + 2);
-            tv[0] = t0.x, tv[1] = t0.y, tv[2] = t1.x, tv[3] = t1.y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            xv[j] = xr[c4 + j];
-            cv[j] = ck[c4 + j];
-            tv[j] = ct ? ct[c4 + j] : 0.0;
-          }
-        }
-        int q[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double y = xv[j] - cv[j];
-          const double v = y * inv;
-          bad |= !(fabs(v) < kQMax);
-          const double tq = __dadd_rn(v, kMagic);
-          const double qd = __dsub_rn(tq, kMagic);
-          q[j] = __double2loint(tq);
-          const double e = y - qd * sc;
-          esum += e * e;
-          ysum += y * y;
-          nsd = fma(qd, qd, nsd);
-          if (ct) {
-            const double dr = xv[j] - tv[j];
-            rsum += dr * dr;
-          }
-        }
-        const uint32_t lw = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
-                                        __byte_perm(q[2], q[3], 0x0040), 0x5410) & 0x7f7f7f7fu;
-        const uint32_t mw = __byte_perm(__byte_perm(q[0] >> kLimb, q[1] >> kLimb, 0x0040),
-                                        __byte_perm(q[2] >> kLimb, q[3] >> kLimb, 0x0040),
-                                        0x5410) & 0x7f7f7f7fu;
-        const uint32_t hw = __byte_perm(
-            __byte_perm(q[0] >> (2 * kLimb), q[1] >> (2 * kLimb), 0x0040),
-            __byte_perm(q[2] >> (2 * kLimb), q[3] >> (2 * kLimb), 0x0040), 0x5410);
-        msq = __dp4a(mw, mw, msq);
-        lsq = __dp4a(lw, lw, lsq);
-        *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
-        *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
-        *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
-      }
-    }
-    unsigned long long nsum = (unsigned long long)nsd;
-    const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
-    if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
-    // generic path: the tail columns (or the whole row when redo / padding)
-    for (int64_t c4 = 4 * hl; c4 < kpad; c4 += 64) {
-      if (!redo && valid && c4 + 4 <= d) continue;
-      uint32_t hw = 0, mw = 0, lw = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t c = c4 + j;
-        int q = 0;
-        if (valid && c < d) {
-          const double x = xr[c];
-          const double y = x - ck[c];
-          double qd = rint(y * inv);
-          qd = fmin(fmax(qd, -kQMax), kQMax);
-          q = (int)qd;
-          const double e = y - qd * sc;
-          esum += e * e;
-          ysum += y * y;
-          if (ct) {
-            const double dr = x - ct[c];
-            rsum += dr * dr;
-          }
-        }
-        nsum += (unsigned long long)((long long)q * q);
-        const uint32_t mq = (q >> kLimb) & ((1 << kLimb) - 1), lq = q & ((1 << kLimb) - 1);
-        msq += mq * mq;
-        lsq += lq * lq;
-        hw |= (uint32_t)(uint8_t)(int8_t)(q >> (2 * kLimb)) << (8 * j);
-        mw |= mq << (8 * j);
-        lw |= lq << (8 * j);
-      }
-      *reinterpret_cast<uint32_t*>(hrow_p + c4) = hw;
-      *reinterpret_cast<uint32_t*>(mrow_p + c4) = mw;
-      *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
-    }
+    const QRow qr = quantize_row(xr, ck, ct, valid, d, kpad, sc, inv, planes + p * kpad,
+                                 planes + P * kpad + p * kpad, planes + 2 * P * kpad + p * kpad,
+                                 hl, half);
+    const unsigned long long nsum = qr.nsum;
+    const uint32_t msq = qr.msq, lsq = qr.lsq;
+    const double esum = qr.esum, ysum = qr.ysum, rsum = qr.rsum;
     // every half-warp is done with this stage: refill it
     __syncthreads();
     if (warp == 0 && i + n_stages < n_it) {
@@ -1000,16 +1033,6 @@ quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_
       issue(i + n_stages, slot);
     }
     if (++slot == n_stages) slot = 0, phase ^= 1u;
-    // row sums over the 16 lanes of the half-warp
-#pragma unroll
-    for (int o = 8; o; o >>= 1) {
-      esum += __shfl_xor_sync(0xffffffffu, esum, o);
-      ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
-      rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-      nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      msq += __shfl_xor_sync(0xffffffffu, msq, o);
-      lsq += __shfl_xor_sync(0xffffffffu, lsq, o);
-    }
     if (hl == 0) {
       nq[p] = (int64_t)nsum;
       cq[p] = (int32_t)((int64_t)nsum >> kYShift);
@@ -1072,6 +1095,142 @@ quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_
   }
 }
 
+// Warp-private rings (d even): the CTA walks its tiles; each warp quantises 16
+// rows of the current tile two at a time (a half-warp per row), streaming
+// them through its own ring of kWStages two-row stages that lanes 0 and 1
+// fill with one bulk copy per row (the next source rows are looked up one
+// step ahead). No CTA barrier per stage: three per tile, for the centres
+// and the tile maxima.
+constexpr int kWStages = 3;
+constexpr int kQWarpsR = 8;  // blockDim.x == 256
+
+__global__ void __launch_bounds__(256, 2)
+quantize_rows_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_t P,
+                     const double* __restrict__ center, const double* __restrict__ scale,
+                     int8_t* __restrict__ planes, int64_t* __restrict__ nq,
+                     int32_t* __restrict__ cq, unsigned long long* __restrict__ tile_e,
+                     const double* __restrict__ cen, unsigned long long* __restrict__ rad_bits,
+                     uint32_t* __restrict__ limb_sq) {
+  extern __shared__ __align__(128) double q_smem[];
+  __shared__ __align__(8) uint64_t wbar[kQWarpsR][kWStages];
+  __shared__ unsigned long long s_red[5][2 * kQWarpsR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane >> 4, hl = lane & 15;
+  double* const ring = q_smem + (int64_t)warp * kWStages * 2 * d;
+  double* const s_c = q_smem + (int64_t)kQWarpsR * kWStages * 2 * d;  // element, tile centre
+  const int64_t n_tiles = P / kTile;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr int kIt = kTile / (2 * kQWarpsR);  // iterations per tile and warp (8)
+  const int64_t n_it = my_tiles * kIt;
+  auto row_of = [&](int64_t i, int h) -> int64_t {
+    const int64_t tile = blockIdx.x + (i / kIt) * gridDim.x;
+    return tile * kTile + warp * (2 * kIt) + (i % kIt) * 2 + h;
+  };
+  // dataset (or Xg) row of iteration i for lanes 0, 1 (-1: pad / none)
+  auto src_row = [&](int64_t i) -> int64_t {
+    if (lane >= 2 || i >= n_it) return -1;
+    return src.index(row_of(i, lane));
+  };
+  auto issue = [&](int sl, int64_t xr) {  // all lanes of the warp
+    uint64_t* bar = &wbar[warp][sl];
+    const unsigned m = __ballot_sync(0xffffffffu, xr >= 0);
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(__popc(m) * d * 8));
+    __syncwarp();
+    if (xr >= 0) bulk_load(ring + (sl * 2 + lane) * d, src.X + xr * d, (uint32_t)(d * 8), bar);
+  };
+  if (lane == 0) {
+    for (int sl = 0; sl < kWStages; ++sl) mbar_init(&wbar[warp][sl], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  int64_t nx = src_row(0);
+  for (int sl = 0; sl < kWStages && sl < n_it; ++sl) {
+    issue(sl, nx);
+    nx = src_row(sl + 1);
+  }
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t tile = blockIdx.x;
+  for (int64_t tl = 0; tl < my_tiles; ++tl, tile += gridDim.x) {
+    int64_t a = 0, bb = et.n_el;
+    while (bb - a > 1) {
+      const int64_t mid = (a + bb) >> 1;
+      if (et.pbase[mid] <= tile * kTile) a = mid; else bb = mid;
+    }
+    const int k = (int)a;  // tiles never straddle elements
+    const double sc = scale[k], inv = 1.0 / sc;
+    __syncthreads();  // the previous tile's readers of s_c / s_red are done
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+      s_c[c] = center[(int64_t)k * d + c];
+      s_c[d + c] = cen ? cen[tile * d + c] : 0.0;
+    }
+    __syncthreads();
+    unsigned long long w_m = 0, w_l = 0, w_e = 0, w_y = 0, w_r = 0;
+    bool w_valid = false;
+    for (int j = 0; j < kIt; ++j) {
+      const int64_t i = tl * kIt + j;
+      const int64_t p = tile * kTile + warp * (2 * kIt) + j * 2 + half;
+      mbar_wait(&wbar[warp][slot], phase);
+      const bool valid = (p - et.pbase[k]) < et.nrows[k];
+      const QRow qr = quantize_row(ring + (slot * 2 + half) * d, s_c, cen ? s_c + d : nullptr,
+                                   valid, d, kpad, sc, inv, planes + p * kpad,
+                                   planes + P * kpad + p * kpad, planes + 2 * P * kpad + p * kpad,
+                                   hl, half);
+      __syncwarp();  // both rows of the stage are consumed: refill it
+      if (i + kWStages < n_it) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(slot, nx);
+        nx = src_row(i + kWStages + 1);
+      }
+      if (++slot == kWStages) slot = 0, phase ^= 1u;
+      if (hl == 0) {
+        nq[p] = (int64_t)qr.nsum;
+        cq[p] = (int32_t)((int64_t)qr.nsum >> kYShift);
+        w_m = max(w_m, (unsigned long long)qr.msq);  // pads are all-zero rows
+        w_l = max(w_l, (unsigned long long)qr.lsq);
+        if (valid) {
+          auto bits = [](double v) {  // NaN -> the positive quiet NaN (max)
+            return (unsigned long long)__double_as_longlong(
+                v == v ? v : __longlong_as_double(0x7ff8000000000000ll));
+          };
+          w_e = max(w_e, bits(qr.esum));
+          w_y = max(w_y, bits(qr.ysum));
+          w_r = max(w_r, bits(qr.rsum));
+          w_valid = true;
+        }
+      }
+    }
+    // tile maxima (see quantize_kernel): one atomic per tile and array
+    if (hl == 0) {
+      const int h2 = 2 * warp + half;
+      s_red[0][h2] = w_m, s_red[1][h2] = w_l;
+      s_red[2][h2] = w_valid ? w_e + 1 : 0;
+      s_red[3][h2] = w_y;
+      s_red[4][h2] = w_r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m[5] = {0, 0, 0, 0, 0};
+      for (int x = 0; x < 5; ++x)
+        for (int w = 0; w < 2 * kQWarpsR; ++w) m[x] = max(m[x], s_red[x][w]);
+      atomicMax(limb_sq + 2 * tile, (uint32_t)m[0]);
+      atomicMax(limb_sq + 2 * tile + 1, (uint32_t)m[1]);
+      if (m[2]) {
+        const double es = __longlong_as_double((long long)(m[2] - 1));
+        const double ys = __longlong_as_double((long long)m[3]);
+        const double e = sqrt(es) * (1.0 + 1e-12) + 1e-15 * sqrt(ys) + 1e-300;
+        atomicMax(tile_e + tile, (unsigned long long)__double_as_longlong(
+                                     e == e ? e : __longlong_as_double(0x7ff8000000000000ll)));
+        if (rad_bits) {
+          const double rr = sqrt(__longlong_as_double((long long)m[4]));
+          atomicMax(rad_bits + tile, (unsigned long long)__double_as_longlong(
+                                         rr == rr ? rr : __longlong_as_double(0x7ff8000000000000ll)));
+        }
+      }
+    }
+  }
+}
+
 // per tile: quantisation-error bound in quantised units; per element: the
 // eps radii a_in = eps/(1+gamma)/s, a_out = eps/(1-gamma)/s
 __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ tile_e_bits,
@@ -1102,17 +1261,21 @@ __global__ void thresholds_prep_kernel(const unsigned long long* __restrict__ ti
 // ---------------------------------------------------------------------------
 // Direction-bound projections from the limb planes (int8 mma.sync): per
 // grouped row tile I (seed a) and every seed g of its element k,
-//   proj[I][g] = s_k * min_{x in I} <q_x, u'_ag> - e_I |u'_ag|   (rounded down)
+//   proj[I][g] = s_k (min_{x in I} <2^14 H_x + 2^7 M_x, u'_ag> - Lmax_I |u'_ag|)
+//                - e_I |u'_ag|                                 (rounded down)
 // where u'_ag = s'_a - s'_g is the difference of the element's int8-quantised
-// seeds (dbscan.cu seed_quant_kernel) and e_I bounds |x - c_k - s_k q_x| over
-// the tile (quantize_kernel). For every direction u,
+// seeds (dbscan.cu seed_quant_kernel), q_x = 2^14 H + 2^7 M + L the row's
+// limbs, Lmax_I = max_x |L_x| (limb norms, quantize_kernel; then
+// <L_x, u'> >= -Lmax_I |u'|, ~2^-14 of the H term) and e_I bounds
+// |x - c_k - s_k q_x| over the tile. For every direction u,
 //   <x, u> = <c_k, u> + s_k <q_x, u> + <e_x, u>,
 // so proj[I][g] + <c_k, u'_ag> <= min_x <x, u'_ag>. In tile_prune_kernel the
 // two tiles of a pair use u'_ab and u'_ba = -u'_ab, the <c_k, u'> terms
 // cancel, and (proj[I][b] + proj[J][a]) / |u'_ab| <= |x - y| for every x in
-// I, y in J. <q_x, s'_g> is exact: the H, M, L limb products accumulate in
-// int32 (|.| <= 128 * 127 * 256) and combine in int64 (2^14 H + 2^7 M + L).
-// One CTA per row tile, 8 warps x 16 rows, all 64 seeds (8 n-tiles).
+// I, y in J. <H_x, s'_g>, <M_x, s'_g> are exact int32 sums (|.| <= 128 * 127
+// * 256), combined in int64. One CTA per row tile, 8 warps x 16 rows, all 64
+// seeds (8 n-tiles); the next K step's A fragments load while this one's MMAs
+// run.
 // ---------------------------------------------------------------------------
 constexpr int kPjSeeds = 64;
 
@@ -1132,7 +1295,7 @@ tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables 
                        const int8_t* __restrict__ seeds_q, const double* __restrict__ unorm,
                        const double* __restrict__ scale,
                        const unsigned long long* __restrict__ tile_e,
-                       double* __restrict__ proj) {
+                       const uint32_t* __restrict__ limb_sq, double* __restrict__ proj) {
   constexpr int kpad = NKC * kKC;
   constexpr int kS = kpad + 16;  // padded smem row: conflict-free B fragments
   __shared__ __align__(16) int8_t sS[kPjSeeds * kS];
@@ -1142,6 +1305,24 @@ tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables 
   if (a < 0) return;  // block-uniform: element not grouped
   const int k = tile_elem[rt];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int r0 = w * 16 + gid;  // this thread's rows: r0, r0 + 8
+  const int64_t p0 = rt * kTile;
+  // A fragments (H and M planes) of K step ks: rows r0 / r0 + 8, bytes
+  // 4 tig.. and 4 tig + 16.. of the step's 32
+  const int8_t* arow = planes + (p0 + r0) * (int64_t)kpad + tig * 4;
+  auto load_a = [&](int ks, uint32_t (&af)[2][4]) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const int8_t* b = arow + (int64_t)l * P * kpad + ks * 32;
+      af[l][0] = __ldg(reinterpret_cast<const uint32_t*>(b));
+      af[l][1] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad));
+      af[l][2] = __ldg(reinterpret_cast<const uint32_t*>(b + 16));
+      af[l][3] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad + 16));
+    }
+  };
+  uint32_t afc[2][4];
+  load_a(0, afc);  // in flight while the seeds are staged
   const int8_t* sk = seeds_q + (int64_t)k * kPjSeeds * kpad;
   for (int i = t; i < kPjSeeds * kpad / 16; i += 256) {
     const int g = i / (kpad / 16), c = i % (kpad / 16);
@@ -1149,44 +1330,39 @@ tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables 
         reinterpret_cast<const int4*>(sk + (int64_t)g * kpad)[c];
   }
   __syncthreads();
-  const int64_t p0 = rt * kTile;
   const int valid = min(kTile, (int)(et.nrows[k] - (p0 - et.pbase[k])));
-  const int gid = lane >> 2, tig = lane & 3;
-  const int r0 = w * 16 + gid;  // this thread's rows: r0, r0 + 8
-  int acc[3][8][4];
+  int acc[2][8][4];
 #pragma unroll
-  for (int l = 0; l < 3; ++l)
+  for (int l = 0; l < 2; ++l)
 #pragma unroll
     for (int n = 0; n < 8; ++n)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[l][n][j] = 0;
-  const int8_t* arow = planes + (p0 + r0) * (int64_t)kpad + tig * 4;
-#pragma unroll 2
-  for (int ks = 0; ks < kpad / 32; ++ks) {
-    uint32_t af[3][4];
 #pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const int8_t* b = arow + (int64_t)l * P * kpad + ks * 32;
-      af[l][0] = __ldg(reinterpret_cast<const uint32_t*>(b));
-      af[l][1] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad));
-      af[l][2] = __ldg(reinterpret_cast<const uint32_t*>(b + 16));
-      af[l][3] = __ldg(reinterpret_cast<const uint32_t*>(b + 8 * kpad + 16));
-    }
+  for (int ks = 0; ks < kpad / 32; ++ks) {
+    uint32_t afn[2][4];
+    if (ks + 1 < kpad / 32) load_a(ks + 1, afn);
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
       const int8_t* bp = sS + (n * 8 + gid) * kS + ks * 32 + tig * 4;
       const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bp);
       const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bp + 16);
 #pragma unroll
-      for (int l = 0; l < 3; ++l) mma_s8_16832(acc[l][n], af[l], b0, b1);
+      for (int l = 0; l < 2; ++l) mma_s8_16832(acc[l][n], afc[l], b0, b1);
+    }
+    if (ks + 1 < kpad / 32) {
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) afc[l][j] = afn[l][j];
     }
   }
-  // <q_x, s'_g> of row r0 (j = 0, 1) or r0 + 8 (j = 2, 3), column n * 8 + 2 tig + (j & 1)
-#define BM_PJ_COMB(n, j)                                                        \
-  ((long long)acc[0][n][j] * (1ll << (2 * kLimb)) + (long long)acc[1][n][j] * (1 << kLimb) + \
-   (long long)acc[2][n][j])
-  // <q_x, s'_a> of my two rows, from the lane of the same row group owning column a
-  // (static register indices only: selects, no dynamically indexed arrays)
+  // <2^14 H_x + 2^7 M_x, s'_g> of row r0 (j = 0, 1) or r0 + 8 (j = 2, 3),
+  // column n * 8 + 2 tig + (j & 1)
+#define BM_PJ_COMB(n, j) \
+  ((long long)acc[0][n][j] * (1ll << (2 * kLimb)) + (long long)acc[1][n][j] * (1 << kLimb))
+  // <., s'_a> of my two rows, from the lane of the same row group owning
+  // column a (static register indices only: selects, no indexed arrays)
   const int na = a >> 3, ca = a & 7;
   const bool odd = ca & 1;
   long long da_lo = 0, da_hi = 0;
@@ -1219,7 +1395,10 @@ tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables 
     for (int i = 1; i < 8; ++i) m = min(m, red[i][t]);
     const double e = __longlong_as_double((long long)tile_e[rt]);
     const double u = unorm[((int64_t)k * kPjSeeds + a) * kPjSeeds + t];
-    double v = __dsub_rd(__dmul_rd(scale[k], (double)m), __dmul_ru(e, u));
+    const double lmax = __dsqrt_ru((double)limb_sq[2 * rt + 1]);
+    // s_k (m - Lmax |u'|) - e |u'|, every step rounded down
+    const double inner = __dsub_rd((double)m, __dmul_ru(lmax, u));
+    double v = __dsub_rd(__dmul_rd(scale[k], inner), __dmul_ru(e, u));
     if (!(e == e) || m == kMax || !(v == v)) v = -1.0e300;  // NaN/inf rows: no bound
     proj[rt * kPjSeeds + t] = v;
   }
@@ -1550,7 +1729,16 @@ int tc_prepare(const RowSrc src, int64_t d, const ElemTables& et, int64_t P, dou
   if (rad) BM_CHECK_CUDA(cudaMemsetAsync(rad, 0, n_tiles * 8, stream));
   BM_TRY(scratch_alloc(tp->s_lim, (size_t)n_tiles * 8, stream));
   BM_CHECK_CUDA(cudaMemsetAsync(tp->s_lim.ptr, 0, n_tiles * 8, stream));
-  {
+  if (d % 2 == 0) {  // per-row bulk copies (16-byte multiples) into warp-private rings
+    const size_t smem = ((size_t)kQWarpsR * kWStages * 2 * d + 2 * d) * 8;
+    BM_TRY(ensure_dyn_smem((const void*)quantize_rows_kernel, (int)smem));
+    quantize_rows_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * 2), 256,
+                           smem, stream>>>(
+        src, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
+        reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),
+        cen, reinterpret_cast<unsigned long long*>(rad), tp->s_lim.as<uint32_t>());
+    BM_CHECK_LAUNCH();
+  } else {
     const int64_t stage = (int64_t)kQRows * d * 8;
     const int n_stages = (int)std::min<int64_t>(kQMaxStages, (kQSmem - 16 * d) / stage);
     BM_REQUIRE(n_stages >= 2, "quantiser ring: d=%lld too large", (long long)d);
@@ -1592,11 +1780,11 @@ int tc_tile_project(TcPrep* tp, const ElemTables& et, const int32_t* tseed,
   if (tp->nkc == 1)
     tile_project_i8_kernel<1><<<grid, 256, 0, stream>>>(
         tp->s_pl.as<int8_t>(), tp->P, et, tp->d_tile_elem, tseed, seeds_q, unorm, scale,
-        tp->s_te.as<unsigned long long>(), proj);
+        tp->s_te.as<unsigned long long>(), tp->s_lim.as<uint32_t>(), proj);
   else
     tile_project_i8_kernel<2><<<grid, 256, 0, stream>>>(
         tp->s_pl.as<int8_t>(), tp->P, et, tp->d_tile_elem, tseed, seeds_q, unorm, scale,
-        tp->s_te.as<unsigned long long>(), proj);
+        tp->s_te.as<unsigned long long>(), tp->s_lim.as<uint32_t>(), proj);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }

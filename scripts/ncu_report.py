@@ -59,7 +59,12 @@ for k in range(len(r) - 2):
             return float(v)
         except ValueError:
             return None
-    data = [x for x in rows[2:] if len(x) >= len(hdr) - 1 and f(x[ix[key]]) is not None]
+    # the source page lists each SASS line once per view: keep one copy
+    seen, data = set(), []
+    for x in rows[2:]:
+        if len(x) >= len(hdr) - 1 and f(x[ix[key]]) is not None and tuple(x) not in seen:
+            seen.add(tuple(x))
+            data.append(x)
     tot = sum(f(x[ix[key]]) for x in data) or 1.0
     stalls = [n for n in hdr if n.startswith("stall_") and "Not Issued" not in n]
     print("=" * 100)

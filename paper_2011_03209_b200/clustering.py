@@ -184,10 +184,28 @@ def labels_to_clusterings(rows_h: np.ndarray, offsets: np.ndarray, labels_h: np.
             cuts = np.searchsorted(lab_sorted, np.arange(int(ncl[k]) + 1))
             clusters = [rows_sorted[cuts[c]:cuts[c + 1]].tolist() for c in range(int(ncl[k]))]
         else:
+            rows_sorted, cuts = r[:0], np.zeros(1, dtype=np.int64)
             clusters = []
         noise = r[lab < 0].tolist()
-        out.append(PullbackClustering(k, clusters, noise))
+        pbc = PullbackClustering(k, clusters, noise)
+        # flat copy for build_graph's fast path (no list -> array conversion);
+        # only used while pbc.clusters still holds these very lists
+        pbc._flat = (rows_sorted[cuts[0]:cuts[-1]], np.diff(cuts), id(clusters),
+                     [(id(c), len(c)) for c in clusters])
+        out.append(pbc)
     return out
+
+
+def flat_clusters(pbc):
+    """(rows in cluster order, cluster sizes) of a PullbackClustering made by
+    cluster_all, or None if its cluster lists were replaced or resized."""
+    f = getattr(pbc, "_flat", None)
+    if f is None or f[2] != id(pbc.clusters) or len(pbc.clusters) != len(f[3]):
+        return None
+    for c, (ic, ln) in zip(pbc.clusters, f[3]):
+        if id(c) != ic or len(c) != ln:
+            return None
+    return f[0], f[1]
 
 
 def cluster_all(pc, memberships: list, params: DbscanParams, strategy: DistanceStrategy,

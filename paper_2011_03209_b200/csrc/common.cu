@@ -2,6 +2,7 @@
 #include <stdarg.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -91,11 +92,16 @@ void trace_dump() {
   m.clear();
 }
 
+size_t big_idle_bytes(int dev);
+
 int device_free_bytes(size_t* free_b) {
   size_t total = 0;
   BM_CHECK_CUDA(cudaMemGetInfo(free_b, &total));
   int dev = 0;
   cudaGetDevice(&dev);
+  // idle cached large buffers are reusable too: counting them keeps the
+  // window plan of a huge element the same from call to call
+  *free_b += big_idle_bytes(dev);
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t reserved = 0, used = 0;
@@ -135,9 +141,29 @@ void big_free_locked(BigBuf& b) {  // g_big_mu held; b idle
 }
 }  // namespace
 
+// Size classes of the cached buffers: requests are rounded up to 1/16 of
+// their power-of-two magnitude (<= 6.25% over-allocation), so a request that
+// varies slightly between calls (window plans follow the free memory) reuses
+// the cached buffer instead of mapping tens of GB afresh.
+static size_t big_class(size_t bytes) {
+  size_t p2 = 1;
+  while (p2 < bytes) p2 <<= 1;
+  const size_t g = std::max<size_t>(p2 >> 4, (size_t)1 << 20);
+  return (bytes + g - 1) / g * g;
+}
+
+size_t big_idle_bytes(int dev) {
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  size_t b = 0;
+  for (const auto& x : g_big)
+    if (!x.busy && x.p && x.dev == dev) b += x.bytes;
+  return b;
+}
+
 int big_acquire(size_t bytes, cudaStream_t stream, void** out, int* slot) {
   int dev = 0;
   cudaGetDevice(&dev);
+  bytes = big_class(bytes);
   std::lock_guard<std::mutex> lk(g_big_mu);
   int best = -1;
   for (int i = 0; i < (int)g_big.size(); ++i) {
@@ -226,6 +252,11 @@ int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
   s.stream = stream;
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMallocAsync(&s.ptr, bytes, stream);
+  if (e != cudaSuccess) {  // idle cached large buffers hold the memory: free them, retry
+    cudaGetLastError();
+    big_trim();
+    e = cudaMallocAsync(&s.ptr, bytes, stream);
+  }
   if (e != cudaSuccess) {
     s.ptr = nullptr;
     cudaGetLastError();

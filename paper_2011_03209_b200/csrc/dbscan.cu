@@ -2144,10 +2144,14 @@ extern "C" int bm_cluster_elements(const double* d_X, int64_t n, int64_t d,
       int32_t* d_out = d_labels + h_offsets[bt.k0];
       std::vector<std::pair<int32_t, int32_t>> wins;
       if (bt.windowed) {
+        // the window plan is a function of the device size (not of the free
+        // memory of the moment), so repeated calls reuse the cached bitmap
+        // buffer: at most 45% of the device, less if it is not free
         size_t free_now = 0;
         BM_TRY(device_free_bytes(&free_now));
-        int64_t cap = (int64_t)((0.85 * (double)free_now - (double)(2ll << 30)) /
-                                (kTileWords * 4.0 + kTileAux));
+        const double avail = std::min(0.45 * (double)device_total_bytes(),
+                                      0.85 * (double)free_now - (double)(2ll << 30));
+        int64_t cap = (int64_t)(avail / (kTileWords * 4.0 + kTileAux));
         if (forced_cap > 0) cap = forced_cap;  // windows still hold >= 1 tile row
         wins = row_windows(bc, std::max<int64_t>(cap, 1));
       } else {

@@ -76,6 +76,22 @@ def test_pca2d_library_pieces(golden):
     cl = cluster_all(pc, members, DbscanParams(q["eps"], q["min_pts"]), DistanceStrategy())
     g = build_graph(cl, pc, fv, cover, manifest={"test": True})
     assert graph_to_json(g) == z["graph"].tobytes()
+    # build_graph's flat fast path (lists made by cluster_all) and the generic
+    # path (caller-built lists; one edited in place) give the same bytes
+    import copy
+
+    from paper_2011_03209_b200.clustering import flat_clusters
+
+    assert all(flat_clusters(c) is not None for c in cl)
+    cl2 = copy.deepcopy(cl)
+    assert all(flat_clusters(c) is None for c in cl2 if c.clusters)
+    assert graph_to_json(build_graph(cl2, pc, fv, cover, manifest={"test": True})) == \
+        z["graph"].tobytes()
+    k = next(i for i, c in enumerate(cl) if c.clusters)
+    cl[k].clusters[0].append(cl[k].clusters[0].pop())  # same length, same content
+    cl[k].clusters.append([])  # resized: the generic path for element k
+    assert flat_clusters(cl[k]) is None
+    cl[k].clusters.pop()
 
 
 def test_modes_and_thresholds_identical_when_no_ties():

@@ -1101,10 +1101,10 @@ quantize_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_
 // fill with one bulk copy per row (the next source rows are looked up one
 // step ahead). No CTA barrier per stage: three per tile, for the centres
 // and the tile maxima.
-constexpr int kWStages = 3;
+constexpr int kWStages = 2;
 constexpr int kQWarpsR = 8;  // blockDim.x == 256
 
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 quantize_rows_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, int64_t P,
                      const double* __restrict__ center, const double* __restrict__ scale,
                      int8_t* __restrict__ planes, int64_t* __restrict__ nq,
@@ -1732,7 +1732,7 @@ int tc_prepare(const RowSrc src, int64_t d, const ElemTables& et, int64_t P, dou
   if (d % 2 == 0) {  // per-row bulk copies (16-byte multiples) into warp-private rings
     const size_t smem = ((size_t)kQWarpsR * kWStages * 2 * d + 2 * d) * 8;
     BM_TRY(ensure_dyn_smem((const void*)quantize_rows_kernel, (int)smem));
-    quantize_rows_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * 2), 256,
+    quantize_rows_kernel<<<(unsigned)std::min<int64_t>(n_tiles, (int64_t)num_sms() * 3), 256,
                            smem, stream>>>(
         src, d, kpad, et, P, center, scale, tp->s_pl.as<int8_t>(), tp->s_nq.as<int64_t>(),
         reinterpret_cast<int32_t*>(tp->s_nq.as<int64_t>() + P), tp->s_te.as<unsigned long long>(),

@@ -51,6 +51,21 @@ void count_launch();
     }                                \
   } while (0)
 
+// Device-side bounds assertions of the debug build (-DBM_DEBUG_BOUNDS,
+// B200MAP_NVCC_FLAGS): a violated index traps the kernel (the launch's
+// sticky error surfaces as InternalError). Compiled out otherwise.
+#ifdef BM_DEBUG_BOUNDS
+#define BM_DASSERT(cond)                                                          \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      printf("BM_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #cond);         \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define BM_DASSERT(cond) ((void)0)
+#endif
+
 #define BM_REQUIRE_INTERNAL(cond, ...) \
   do {                                 \
     if (!(cond)) {                     \

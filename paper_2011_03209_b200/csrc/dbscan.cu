@@ -1112,6 +1112,7 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
     const int64_t pb = et.pbase[k];
     const int nk = et.nrows[k];
     const int pI = (int)(pb + I * kTile);
+    BM_DASSERT(k >= 0 && k < et.n_el && I >= 0 && I < et.ntiles[k]);
     // row side once per unit (stale roots later only cost redundant unions)
     const bool ci = core[pI + t];
     int gr = ci ? uf_find(par, pI + t) : -1;
@@ -1124,6 +1125,7 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
     for (int s = 0; s < un.cnt; ++s) {
       const int64_t g = un.off + s;
       const int J = tiles[g].J;
+      BM_DASSERT(tiles[g].k == k && tiles[g].I == I && J >= I && J < et.ntiles[k]);
       const int pJ = (int)(pb + J * kTile);
       (void)COMP_STAT(0);
       if (!DIAG) {

@@ -85,6 +85,7 @@ __device__ __forceinline__ void decode_tile(const ElemTables& et, int64_t g, int
 }
 
 __device__ __forceinline__ int uf_find(int* par, int x) {
+  BM_DASSERT(x >= 0);
   while (true) {
     int p = __ldcg(par + x);
     if (p == x) return x;

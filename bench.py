@@ -134,11 +134,15 @@ def alg_flops(sizes, d):
     return float((2.0 * d * s * (s - 1) / 2.0).sum())
 
 
+TRAFFIC_PROFILE = "profiles/r02_ncu_full_cfg3.txt"
+
+
 def ncu_traffic(kernel="tc_adjacency_kernel"):
     """DRAM bytes (read + write) per launch of the dominant kernel from the
-    committed ncu --set full capture (profiles/r01_ncu_full_cfg3.txt)."""
+    committed ncu --set full capture of the same build (TRAFFIC_PROFILE; ncu
+    replays kernels, so it cannot run inside the timed bench)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_cfg3.txt")) as f:
+        with open(os.path.join(ROOT, TRAFFIC_PROFILE)) as f:
             block = None
             for line in f:
                 if line.startswith("void ") or line.startswith("unnamed"):
@@ -642,8 +646,9 @@ def main():
                 "api": e2e_api},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
-                     "traffic_note": "DRAM bytes per tc_adjacency_kernel launch, ncu --set full "
-                                     "(profiles/r01_ncu_full_cfg3.txt)",
+                     "traffic_note": "DRAM bytes per tc_adjacency_kernel launch at cfg3, from "
+                                     "the ncu --set full capture " + TRAFFIC_PROFILE +
+                                     " (not measured in this run)",
                      "kernel": "eps-adjacency (distance tiles) stage",
                      "kernel_ms_per_step": adj_s * 1e3,
                      "kernel_share_of_step": adj_s / (t_dev / args.steps),

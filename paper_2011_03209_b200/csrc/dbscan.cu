@@ -246,13 +246,16 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
 
 // One thread per entry: its first kGroupDims coordinates in registers
 // (fp32), the 64 seeds broadcast from shared memory, 4 dims per 16-byte
-// load; nearest seed (smallest index on ties) -> key (element, seed rank).
-__global__ void __launch_bounds__(128)
+// load; nearest seed by |s|^2 - 2 <x, s> (one FMA per dim; smallest index on
+// ties) -> key (element, seed rank). The grouping only orders rows for the
+// pruning; any assignment gives the same clusters.
+__global__ void __launch_bounds__(128, 6)
 group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                     const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
                     const int32_t* __restrict__ seed_rank, uint64_t* __restrict__ keys,
                     int64_t* __restrict__ vals) {
   __shared__ __align__(16) float sd[kGroupSeeds][kGroupDims];  // seed coordinates
+  __shared__ float sn[kGroupSeeds];                              // |s|^2
   const GroupItem it = items[blockIdx.x];
   const int64_t ek = offs[it.k], nk = offs[it.k + 1] - ek;
   const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
@@ -264,24 +267,28 @@ group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
     sd[j][dim] = v;
   }
   __syncthreads();
+  if (threadIdx.x < kGroupSeeds) {
+    float q = 0.0f;
+    for (int c = 0; c < kGroupDims; ++c) q = fmaf(sd[threadIdx.x][c], sd[threadIdx.x][c], q);
+    sn[threadIdx.x] = q;
+  }
+  __syncthreads();
   for (int e = it.e0 + threadIdx.x; e < it.e1; e += blockDim.x) {
     const double* xr = X + rows[e] * d;
     float x[kGroupDims];
 #pragma unroll
-    for (int c = 0; c < kGroupDims; ++c) x[c] = c < D ? (float)xr[c] : 0.0f;
+    for (int c = 0; c < kGroupDims; ++c) x[c] = c < D ? -2.0f * (float)xr[c] : 0.0f;
     float best = 3.0e38f;
     int bi = 0;
     for (int j = 0; j < S; ++j) {
-      float acc = 0.0f;
+      float acc = sn[j];
 #pragma unroll
       for (int c = 0; c < kGroupDims; c += 4) {
         const float4 sv = *reinterpret_cast<const float4*>(&sd[j][c]);
-        const float a0 = x[c] - sv.x, a1 = x[c + 1] - sv.y, a2 = x[c + 2] - sv.z,
-                    a3 = x[c + 3] - sv.w;
-        acc = fmaf(a0, a0, acc);
-        acc = fmaf(a1, a1, acc);
-        acc = fmaf(a2, a2, acc);
-        acc = fmaf(a3, a3, acc);
+        acc = fmaf(x[c], sv.x, acc);
+        acc = fmaf(x[c + 1], sv.y, acc);
+        acc = fmaf(x[c + 2], sv.z, acc);
+        acc = fmaf(x[c + 3], sv.w, acc);
       }
       if (acc < best) {
         best = acc;

@@ -31,8 +31,12 @@ STRATEGY_MODES = ("precomputed", "on-the-fly")
 
 # Cover elements are clustered in groups of at most this many membership
 # entries per device call so cancel_check is polled between groups
-# (clustering.py:273-274, 296-297).
+# (clustering.py:273-274, 296-297). With a cancel_check, a group also holds at
+# most CANCEL_GROUP_PAIRS of pair work (sum n_k^2, ~0.1 s of device time at
+# cfg3's density), so a second-long build (cfg5) is polled several times;
+# without one, the whole build is one call.
 CANCEL_GROUP_ENTRIES = 4_000_000
+CANCEL_GROUP_PAIRS = 2.0e10
 
 
 def effective_mem_budget() -> int:
@@ -127,16 +131,20 @@ def fill_stats(stats_out: ClusterRunStats | None, sizes, orders, strategy, dev_s
         stats_out.adjacency_bytes = max(stats_out.adjacency_bytes, int(dev_stats[4]))
 
 
-def split_groups(offsets: np.ndarray, limit: int = CANCEL_GROUP_ENTRIES) -> list:
-    """Contiguous element ranges of bounded total size (cancel_check cadence)."""
-    groups, k0, acc = [], 0, 0
+def split_groups(offsets: np.ndarray, limit: int = CANCEL_GROUP_ENTRIES,
+                 pair_limit: float | None = None) -> list:
+    """Contiguous element ranges of bounded total size (cancel_check cadence):
+    at most `limit` entries and, if given, `pair_limit` of sum n_k^2."""
+    groups, k0, acc, pairs = [], 0, 0, 0.0
     n_el = len(offsets) - 1
     for k in range(n_el):
         nk = int(offsets[k + 1] - offsets[k])
-        if acc and acc + nk > limit:
+        if acc and (acc + nk > limit or
+                    (pair_limit is not None and pairs + float(nk) ** 2 > pair_limit)):
             groups.append((k0, k))
-            k0, acc = k, 0
+            k0, acc, pairs = k, 0, 0.0
         acc += nk
+        pairs += float(nk) ** 2
     groups.append((k0, n_el))
     return groups
 
@@ -153,7 +161,8 @@ def cluster_device(X, rows_dev, offsets, params: DbscanParams, orders, cancel_ch
     labels = torch.empty(max(int(offsets[-1]), 1), dtype=torch.int32, device=X.device)
     ncl = np.zeros(n_el, dtype=np.int32)
     stats = np.zeros(8, dtype=np.int64)
-    for k0, k1 in split_groups(offsets):
+    pair_limit = CANCEL_GROUP_PAIRS if cancel_check is not None else None
+    for k0, k1 in split_groups(offsets, CANCEL_GROUP_ENTRIES, pair_limit):
         if cancel_check is not None:
             cancel_check()
         a, b = int(offsets[k0]), int(offsets[k1])

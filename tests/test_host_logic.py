@@ -116,3 +116,16 @@ def test_canonical_float_format():
         b"[1e-05,0,0.1,1.23456789e+11,2.5]"
     with pytest.raises(DataError):
         to_canonical_json([float("nan")])
+
+
+def test_split_groups_pair_work_limit():
+    """With a cancel_check, groups are also bounded by sum n_k^2 (cfg5-scale
+    builds poll several times); an element above the limit is alone."""
+    sizes = [100, 5, 5, 300, 1, 1, 200]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    groups = split_groups(offs, limit=10 ** 9, pair_limit=100 ** 2 + 60)
+    assert [k for a, b in groups for k in range(a, b)] == list(range(len(sizes)))
+    for a, b in groups:
+        work = sum(s * s for s in sizes[a:b])
+        assert b - a == 1 or work <= 100 ** 2 + 60
+    assert split_groups(offs, limit=10 ** 9) == [(0, len(sizes))]

@@ -1100,14 +1100,12 @@ __device__ unsigned long long g_comp_stats[8];
 #endif
 
 template <bool DIAG>
-__global__ void __launch_bounds__(128, 12)
+__global__ void __launch_bounds__(128)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
                   const TileUnit* __restrict__ units, const TileRef* __restrict__ tiles,
                   int64_t slot0, int64_t n_units, const uint8_t* __restrict__ core,
                   int32_t* __restrict__ par, int32_t* __restrict__ bmin,
-                  const int32_t* __restrict__ uni, const int32_t* __restrict__ nonempty,
-                  const int32_t* __restrict__ croot, const uint32_t* __restrict__ cmask,
-                  const uint32_t* __restrict__ tmask) {
+                  const int32_t* __restrict__ uni, const int32_t* __restrict__ nonempty) {
   __shared__ uint32_t bits[kTileWords];
   __shared__ int groot[2 * kTile];  // global root of each tile node (-1: not core)
   __shared__ int lp[2 * kTile];     // local union-find over tile nodes
@@ -1150,27 +1148,6 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
             (void)COMP_STAT(2);
             if (t == 0 && uI != uJ) uf_union(par, uI, uJ);
             continue;  // block-uniform
-          }
-        }
-        if (tmask) {
-          // every bit of the tile joins a core row and a core column (the
-          // rows / columns holding bits, tmask, are all core) and the core
-          // rows of I, the core columns of J each share one root: the tile
-          // can only join those two roots (a nonempty tile does), no border
-          // rule applies, and its bits need not be read
-          const int rI = croot[(pb >> 7) + I], rJ = croot[(pb >> 7) + J];
-          if (rI >= 0 && rJ >= 0) {
-            const uint32_t* tm = tmask + (g - slot0) * 8;
-            const uint32_t* mI = cmask + ((pb >> 7) + I) * 4;
-            const uint32_t* mJ = cmask + ((pb >> 7) + J) * 4;
-            uint32_t dirty = 0;
-#pragma unroll
-            for (int w = 0; w < 4; ++w) dirty |= (tm[w] & ~mI[w]) | (tm[4 + w] & ~mJ[w]);
-            if (!dirty) {
-              (void)COMP_STAT(6);
-              if (t == 0 && rI != rJ) uf_union(par, rI, rJ);
-              continue;  // block-uniform
-            }
           }
         }
       }
@@ -1355,11 +1332,8 @@ bool check_symmetry() {
 
 // per 128-row tile: the common root of its rows if every valid row is core
 // and all share one root (stale roots are fine: still in the component), else -1
-// Also (croot != null): croot[rt] = the common root of the tile's CORE rows
-// (-1: none or several) and cmask[rt] = its core rows as 4 bit words.
 __global__ void tile_uniform_kernel(ElemTables et, int64_t n_rt, const uint8_t* __restrict__ core,
-                                    int32_t* __restrict__ par, int32_t* __restrict__ uni,
-                                    int32_t* __restrict__ croot, uint32_t* __restrict__ cmask) {
+                                    int32_t* __restrict__ par, int32_t* __restrict__ uni) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t rt = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); rt < n_rt;
@@ -1368,13 +1342,8 @@ __global__ void tile_uniform_kernel(ElemTables et, int64_t n_rt, const uint8_t* 
     int mn = 0x7fffffff, mx = -1;
     for (int i = lane; i < kTile; i += 32) {
       const int64_t p = rt * kTile + i;
-      const bool c = et.ent[p] >= 0 && core[p];
-      if (cmask) {
-        const unsigned w = __ballot_sync(0xffffffffu, c);
-        if (lane == 0) cmask[rt * 4 + i / 32] = w;
-      }
       if (et.ent[p] < 0) continue;
-      if (!c) {
+      if (!core[p]) {
         ok = false;
         continue;
       }
@@ -1385,11 +1354,7 @@ __global__ void tile_uniform_kernel(ElemTables et, int64_t n_rt, const uint8_t* 
     ok = __all_sync(0xffffffffu, ok);
     mn = (int)__reduce_min_sync(0xffffffffu, (unsigned)mn);
     mx = __reduce_max_sync(0xffffffffu, mx);
-    const int one = (mx >= 0 && mn == mx) ? mn : -1;
-    if (lane == 0) {
-      uni[rt] = ok ? one : -1;
-      if (croot) croot[rt] = one;
-    }
+    if (lane == 0) uni[rt] = (ok && mx >= 0 && mn == mx) ? mn : -1;
   }
 }
 
@@ -1958,26 +1923,18 @@ struct BatchCtx {
       BM_CHECK_CUDA(cudaStreamSynchronize(stream));
       BM_REQUIRE_INTERNAL(h_bad == 0, "asymmetric diagonal tile bitmap (%llu bits)", h_bad);
     }
-    // per-slot row/column "holds a bit" masks (8 words), from the
-    // tensor-core engine only
-    const uint32_t* tmask = use_tc ? reinterpret_cast<const uint32_t*>(nonempty + w.n_tiles)
-                                   : nullptr;
     if (w.n_diag > 0) {
       components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
-          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty,
-          nullptr, nullptr, nullptr);
+          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty);
       BM_CHECK_LAUNCH();
     }
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
     BM_CHECK_LAUNCH();
     if (w.n_off > 0) {
       Scratch s_uni;
-      BM_TRY(scratch_alloc(s_uni, (size_t)n_rt * 4 * 6, stream));
-      int32_t* croot = s_uni.as<int32_t>() + n_rt;
-      uint32_t* cmask = reinterpret_cast<uint32_t*>(croot + n_rt);
-      tile_uniform_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(
-          et, n_rt, core, par_w, s_uni.as<int32_t>(), tmask ? croot : nullptr,
-          tmask ? cmask : nullptr);
+      BM_TRY(scratch_alloc(s_uni, (size_t)n_rt * 4, stream));
+      tile_uniform_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(et, n_rt, core, par_w,
+                                                                     s_uni.as<int32_t>());
       BM_CHECK_LAUNCH();
 #ifdef BM_COMP_STATS
       {
@@ -1988,7 +1945,7 @@ struct BatchCtx {
 #endif
       components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
           adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w, s_uni.as<int32_t>(),
-          nonempty, croot, cmask, tmask);
+          nonempty);
       BM_CHECK_LAUNCH();
 #ifdef BM_COMP_STATS
       {
@@ -2001,9 +1958,8 @@ struct BatchCtx {
         int64_t nu = 0;
         for (auto v : hu) nu += v >= 0;
         fprintf(stderr, "[comp-stats] off-diag tiles %llu: empty %llu, both-uniform %llu, "
-                "clean (masks) %llu, rmm-uniform %llu, full %llu, merged %llu; uniform row tiles "
-                "%lld / %lld\n", h[0], h[1], h[2], h[6], h[3], h[4], h[5], (long long)nu,
-                (long long)n_rt);
+                "rmm-uniform %llu, full %llu, merged %llu; uniform row tiles %lld / %lld\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], (long long)nu, (long long)n_rt);
       }
 #endif
     }
@@ -2014,8 +1970,7 @@ struct BatchCtx {
   size_t window_bytes(int32_t I0, int32_t I1) const {
     int64_t r0 = 0, r1 = 0;
     rows_of(I0, I1, r0, r1);
-    // bitmap + nonempty flag + row/column masks (8 words) per kept tile
-    return (size_t)std::max<int64_t>(row_first[r1] - row_first[r0], 1) * (kTileWords * 4 + 4 + 32);
+    return (size_t)std::max<int64_t>(row_first[r1] - row_first[r0], 1) * (kTileWords * 4 + 4);
   }
 
   // canonical labels of every entry (element-relative cluster ids, -1 noise)
@@ -2069,7 +2024,7 @@ int64_t row_window_cap() {
 }
 
 // bytes per kept tile besides its bitmap: tile ref, thresholds, recheck queue
-constexpr double kTileAux = 16.0 + 24.0 + 32.0 + 16.0 * 16384.0 / 2000.0;
+constexpr double kTileAux = 16.0 + 24.0 + 16.0 * 16384.0 / 2000.0;
 
 }  // namespace bm
 

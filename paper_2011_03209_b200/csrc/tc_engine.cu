@@ -214,7 +214,6 @@ struct TcParams {
   int nkc;                // Kpad / 128
   uint32_t* adj;
   int32_t* nonempty;      // per window slot: 1 if the tile holds any bit (zeroed by the host)
-  uint32_t* tmask;        // per window slot: rows (4 words), columns (4 words) holding a bit
   int32_t* cnt;           // eps-neighbour counts per padded row (self included)
   int4* queue;            // undecided pairs: (p_i, p_j, slot, element)
   const uint8_t* planes;  // limb planes [3][P][kpad]
@@ -677,17 +676,7 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         // bitmap word (row, 32 columns) of the tile
         BM_DASSERT(tile >= 0 && row < kTile && ch < 4);
         P.adj[tile * kTileWords + row * 4 + ch] = in_w;
-        {
-          // nonempty flag and the row / column masks of the tile (components
-          // skips tiles whose bits all join core rows and core columns)
-          const uint32_t rany = __ballot_sync(0xffffffffu, in_w != 0u);
-          const uint32_t cany = __reduce_or_sync(0xffffffffu, in_w);
-          if (rany && lane == 0) {
-            P.nonempty[tile] = 1;
-            atomicOr(P.tmask + tile * 8 + q, rany);
-            atomicOr(P.tmask + tile * 8 + 4 + ch, cany);
-          }
-        }
+        if (__any_sync(0xffffffffu, in_w != 0u) && lane == 0) P.nonempty[tile] = 1;
         row_count += __popc(in_w);
         EP_MARK(4);
         // undecided pairs -> exact recheck queue (one atomic per warp)
@@ -1424,7 +1413,7 @@ tile_project_i8_kernel(const int8_t* __restrict__ planes, int64_t P, ElemTables 
 
 __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
                                            uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
-                                           uint32_t* __restrict__ tmask, int32_t* __restrict__ cnt,
+                                           int32_t* __restrict__ cnt,
                                            unsigned long long* __restrict__ n_inside) {
   const int k = pr.w;
   BM_DASSERT(k >= 0 && k < et.n_el);
@@ -1435,8 +1424,6 @@ __device__ __forceinline__ void set_inside(const ElemTables& et, int4 pr,
   const int64_t tile = pr.z;
   atomicOr(adj + tile * kTileWords + r * 4 + (c >> 5), 1u << (c & 31));
   nonempty[tile] = 1;
-  atomicOr(tmask + tile * 8 + (r >> 5), 1u << (r & 31));
-  atomicOr(tmask + tile * 8 + 4 + (c >> 5), 1u << (c & 31));
   atomicAdd(cnt + pr.x, 1);
   if (I != J) atomicAdd(cnt + pr.y, 1);  // off-diagonal bits stand for both orders
   atomicAdd(n_inside, 1ull);
@@ -1459,7 +1446,6 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
                    const int4* __restrict__ queue, const unsigned long long* __restrict__ nq_ptr,
                    unsigned long long qcap, double eps,
                    uint32_t* __restrict__ adj, int32_t* __restrict__ nonempty,
-                   uint32_t* __restrict__ tmask_base,
                    int32_t* __restrict__ cnt, const __grid_constant__ PwProgram c_prog_tc,
                    unsigned long long* __restrict__ n_inside) {
   __shared__ double sq_all[kRcWarps][32][33];
@@ -1559,8 +1545,7 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
     }
     if (have) {
       const double s2 = et.order[k] == BM_ORDER_SEQUENTIAL ? s_seq : __dadd_rn(0.0, st[0]);
-      if (__dsqrt_rn(s2) <= eps)
-        set_inside(et, pr, adj, nonempty, tmask_base, cnt, n_inside);
+      if (__dsqrt_rn(s2) <= eps) set_inside(et, pr, adj, nonempty, cnt, n_inside);
     }
   }
 }
@@ -1864,8 +1849,6 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
   const int64_t P = tp->P, d = tp->d;
   const int nkc = tp->nkc;
   if (n_units == 0) return BM_OK;
-  // the window's per-slot row / column masks follow its nonempty flags
-  uint32_t* tmask = reinterpret_cast<uint32_t*>(nonempty + n_tiles);
   Scratch s_cnt, s_tt;
   BigScratch s_q;  // cached across calls: mapping ~100 MB per call costs ~1 ms
   int32_t* cnt_run = cnt;
@@ -1897,7 +1880,6 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
     BM_CHECK_CUDA(cudaMemsetAsync(d_cnt, 0, 16, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(cnt_run, 0, (size_t)P * 4, stream));
     BM_CHECK_CUDA(cudaMemsetAsync(nonempty, 0, (size_t)n_tiles * 4, stream));
-    BM_CHECK_CUDA(cudaMemsetAsync(tmask, 0, (size_t)n_tiles * 32, stream));
     TcParams prm{};
     prm.et = et;
     prm.units = units;
@@ -1914,7 +1896,6 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
     prm.nkc = nkc;
     prm.adj = adj;
     prm.nonempty = nonempty;
-    prm.tmask = tmask;
     prm.cnt = cnt_run;
     prm.queue = s_q.as<int4>();
     prm.planes = tp->s_pl.as<uint8_t>();
@@ -1981,17 +1962,17 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
     switch (tp->depth) {
       case 1:
         recheck_kernel<1><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, tmask, cnt_run, tp->prog,
+                                                            adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;
       case 2:
         recheck_kernel<2><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, tmask, cnt_run, tp->prog,
+                                                            adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;
       default:
         recheck_kernel<4><<<rg, kRcWarps * 32, 0, stream>>>(src, d, et, q, d_cnt, qcap, tp->eps,
-                                                            adj, nonempty, tmask, cnt_run, tp->prog,
+                                                            adj, nonempty, cnt_run, tp->prog,
                                                             d_cnt + 1);
         break;
     }

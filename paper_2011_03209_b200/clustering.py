@@ -205,6 +205,30 @@ def labels_to_clusterings(rows_h: np.ndarray, offsets: np.ndarray, labels_h: np.
     return out
 
 
+def grouped_clusterings(rows_h: np.ndarray, offsets: np.ndarray, labels_h: np.ndarray,
+                        ncl: np.ndarray, node_rows_h: np.ndarray, node_off_h: np.ndarray) -> list:
+    """Per-element PullbackClustering lists from the device's node grouping
+    (bm_group_nodes: rows of every cluster, ascending, in (element, cluster)
+    order) — the host only slices; noise rows come from one mask pass."""
+    n_el = len(offsets) - 1
+    noise_idx = np.flatnonzero(labels_h < 0)
+    nb = np.searchsorted(noise_idx, offsets)
+    node0 = np.zeros(n_el + 1, dtype=np.int64)
+    np.cumsum(np.asarray(ncl, dtype=np.int64), out=node0[1:])
+    out = []
+    for k in range(n_el):
+        v0, v1 = int(node0[k]), int(node0[k + 1])
+        a, b = int(node_off_h[v0]), int(node_off_h[v1])
+        flat = node_rows_h[a:b]
+        sizes = np.diff(node_off_h[v0:v1 + 1])
+        clusters = [flat[node_off_h[v] - a:node_off_h[v + 1] - a].tolist() for v in range(v0, v1)]
+        noise = rows_h[noise_idx[nb[k]:nb[k + 1]]].tolist()
+        pbc = PullbackClustering(k, clusters, noise)
+        pbc._flat = (flat, sizes, id(clusters), [(id(c), len(c)) for c in clusters])
+        out.append(pbc)
+    return out
+
+
 def flat_clusters(pbc):
     """(rows in cluster order, cluster sizes) of a PullbackClustering made by
     cluster_all, or None if its cluster lists were replaced or resized."""
@@ -251,7 +275,11 @@ def cluster_all(pc, memberships: list, params: DbscanParams, strategy: DistanceS
     rows_dev = torch.from_numpy(rows_h).to(dev)
     labels, ncl, st = cluster_device(X, rows_dev, offsets, params, orders, cancel_check, engine)
     fill_stats(stats_out, sizes, orders, strategy, st)
-    return labels_to_clusterings(rows_h, offsets, labels.cpu().numpy(), ncl)
+    from . import engine as eng
+
+    node_rows, node_off, _ = eng.group_nodes(rows_dev, offsets, labels, ncl)
+    return grouped_clusterings(rows_h, offsets, labels.cpu().numpy(), ncl,
+                               node_rows.cpu().numpy(), node_off.cpu().numpy())
 
 
 def dbscan_rows(pc, rows, params: DbscanParams, order: int = _native.ORDER_SEQUENTIAL,

@@ -568,7 +568,14 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
     TileUnit un_nx = blockIdx.x < P.n_units ? P.units[blockIdx.x] : TileUnit{0, 0, 0, 0};
     int pb_nx = P.et.pbase[un_nx.k], nk_nx = P.et.nrows[un_nx.k];
     int32_t cq_nx = (int32_t)(P.nq[pb_nx + un_nx.I * kBM + row] >> kYShift);
+#ifdef BM_TC_PROFILE
+    long long tu_end = clock64();  // end of the previous unit's last tile
+    ep[5] = 0;
+#endif
     for (int64_t u = blockIdx.x; u < P.n_units; u += gridDim.x) {
+#ifdef BM_TC_PROFILE
+      const long long tu0 = clock64();
+#endif
       const TileUnit un = un_nx;
       const int k = un.k;
       const int pb = pb_nx;
@@ -583,6 +590,10 @@ tc_adjacency_kernel(const __grid_constant__ CUtensorMap qmap, TcParams P) {
         cq_nx = (int32_t)(P.nq[pb_nx + un_nx.I * kBM + row] >> kYShift);
       }
       int row_count = 0;
+#ifdef BM_TC_PROFILE
+      ep[5] += clock64() - tu0;  // unit setup (descriptor + next-unit prefetch)
+      (void)tu_end;
+#endif
       for (int t = 0; t < un.cnt; ++t) {
         const int64_t tile = un.off + t - P.slot0;    // window slot of the kept tile
         // Integer decision. With y = 2^7 a0 + a1 + (a2 >> 7) - floor(N_j/U):
@@ -1939,7 +1950,7 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
       for (int b = 0; b < 148; ++b)
         for (int i = 0; i < 8; ++i) e[i] += pr[148 * 8 + b * 8 + i];
       fprintf(stderr, "[tc-profile] epilogue warp: wait acc01 %.1f%%  E1 %.1f%%  wait acc2 %.1f%%  "
-              "fold %.1f%%  decide+pack %.1f%%  epi_bar %.1f%%  flush+queue %.1f%%  rest %.1f%%\n",
+              "fold %.1f%%  decide+pack %.1f%%  unit setup %.1f%%  flush+queue %.1f%%  rest %.1f%%\n",
               100 * e[0] / e[7], 100 * e[2] / e[7], 100 * e[1] / e[7], 100 * e[3] / e[7],
               100 * e[4] / e[7], 100 * e[5] / e[7], 100 * e[6] / e[7],
               100 * (e[7] - e[0] - e[1] - e[2] - e[3] - e[4] - e[5] - e[6]) / e[7]);

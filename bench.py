@@ -229,6 +229,7 @@ class RefSampler:
         self.secs = np.zeros(len(self.members))
         self.wall = 0.0
         self.r = 0
+        self.n_steps = 0
 
     def step(self, target_s, seed):
         from oracle import ref_timing as RT
@@ -239,6 +240,7 @@ class RefSampler:
         self.rows += res["rows"]
         self.secs += res["seconds"]
         self.wall += res["wall"]
+        self.n_steps += 1
         return res["wall"]
 
     def critical(self, target_s):
@@ -276,15 +278,18 @@ class RefSampler:
         bound = max(crit, float(el.sum()) / self.workers)
         wall = self.t_lens_cover + bound
         pair_dims = float((self.rows * self.sizes).sum()) * self.w.d
-        frac = float((self.rows * self.sizes).sum() / max((self.sizes.astype(float) ** 2).sum(), 1))
+        # pair work sampled per step, as a fraction of one build's
+        frac = float((self.rows * self.sizes).sum() / max(self.n_steps, 1) /
+                     max((self.sizes.astype(float) ** 2).sum(), 1))
         return {
             "value": self.w.n / wall, "unit": UNIT, "cores": self.workers, "kind": "port",
             "seconds_full_build": wall,
             "sample": (f"nervemap's CPU path (oracle/ref_timing.py: cdist rows, count_nonzero, "
                        f"BFS neighbour queries + per-neighbour loop); every one of the "
                        f"{int((self.sizes > 0).sum())} cover elements of {self.w.name} sampled on "
-                       f"{self.workers} busy processes ({int(self.rows.max())} rows per element "
-                       f"max, {100 * frac:.3f}% of the n_k^2 pair work, {self.wall:.1f}s wall; "
+                       f"{self.workers} busy processes ({self.n_steps} samples of up to "
+                       f"{self.r} rows per element, {100 * frac:.3f}% of the n_k^2 pair work "
+                       f"each, {self.wall:.1f}s wall; "
                        f"element time = measured per-row time x n_k), the largest element "
                        f"({int(self.sizes[k])} rows) also sampled alone ({rr} rows): "
                        f"{wall:.0f}s build = lens+cover {self.t_lens_cover:.1f}s (measured, full "

@@ -159,10 +159,11 @@ def cached_device_array(owner, arr: np.ndarray, dev):
     import weakref
 
     key = (id(owner), dev.index)
-    sig = (id(arr), arr.__array_interface__["data"][0], arr.shape, arr.dtype.str)
     with _DEV_CACHE_LOCK:
         hit = _DEV_CACHE.get(key)
-        if hit is not None and hit[0]() is owner and hit[1] == sig:
+        # the entry holds the host array itself: while cached it cannot be
+        # freed, so `is` identifies it (no id/address reuse)
+        if hit is not None and hit[0]() is owner and hit[1] is arr:
             return hit[2]
     t = to_device_f64(arr, dev)
     try:
@@ -170,7 +171,7 @@ def cached_device_array(owner, arr: np.ndarray, dev):
     except TypeError:  # not weak-referenceable: no caching
         return t
     with _DEV_CACHE_LOCK:
-        _DEV_CACHE[key] = (ref, sig, t)
+        _DEV_CACHE[key] = (ref, arr, t)
     return t
 
 

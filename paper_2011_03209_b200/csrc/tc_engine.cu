@@ -831,7 +831,8 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
   constexpr double kQMax = (double)((1 << kQBits) - 1);
   const bool vec = (d & 1) == 0;  // 16-byte aligned rows
   uint32_t msq = 0, lsq = 0;  // |M|^2, |L|^2 of the row's limb planes (exact)
-  double esum = 0.0, ysum = 0.0, rsum = 0.0, nsd = 0.0;
+  double esum = 0.0, ysum = 0.0, rsum = 0.0;
+  long long nsi = 0;
   // Fast path (full 4-column groups of a valid row): rint and the integer
   // conversion by the 1.5 * 2^52 trick (exact rint, ties to even, for
   // |v| < 2^51), byte packing with PRMT, limb norms with DP4A, sum q^2 in
@@ -872,8 +873,7 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
         q[j] = __double2loint(tq);
         const double e = y - qd * sc;
         esum += e * e;
-        ysum += y * y;
-        nsd = fma(qd, qd, nsd);
+        nsi += (long long)q[j] * q[j];  // exact, on the integer pipe
         if (ct) {
           const double dr = xv[j] - tv[j];
           rsum += dr * dr;
@@ -894,7 +894,11 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
       *reinterpret_cast<uint32_t*>(lrow_p + c4) = lw;
     }
   }
-  unsigned long long nsum = (unsigned long long)nsd;
+  // fast path: every |y| < qmax * s, so sum y^2 < d (qmax s)^2 bounds the
+  // row's term of the tile error bound (1e-15 sqrt(max ysum), see the tile
+  // maxima) without a multiply-add per coordinate
+  unsigned long long nsum = (unsigned long long)nsi;
+  if (valid) ysum = (double)d * (kQMax * sc) * (kQMax * sc) * (1.0 + 1e-12);
   const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
   if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
   // generic path: the tail columns (or the whole row when redo / padding)

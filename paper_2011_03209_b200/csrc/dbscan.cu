@@ -39,6 +39,7 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
               int64_t pairs, uint32_t* adj, int32_t* nonempty, int32_t* cnt, bool accumulate,
               bool sync_check, int64_t* stats, cudaStream_t stream);
 void tc_set_queue_scale(TcPrep* tp, double s);
+void tc_set_min_pts(TcPrep* tp, int32_t m);
 int tc_collect(TcPrep* tp, int64_t* rechecked, bool* overflow, cudaStream_t stream);
 int tc_tile_project(TcPrep* tp, const ElemTables& et, const int32_t* tseed,
                     const int8_t* seeds_q, const double* unorm, double* proj,
@@ -1720,6 +1721,7 @@ struct BatchCtx {
       const double* tmm = s_mm.ptr ? s_mm.as<double>() : nullptr;
       BM_TRY(tc_prepare(src, d, et, P, eps, nrows, stream, &tc, cen, rad, tmm));
       tc_set_queue_scale(tc, qscale);
+      tc_set_min_pts(tc, min_pts);
     }
 
     // ---- kept tile pairs and work units (device-built)

@@ -1572,10 +1572,22 @@ __global__ void __launch_bounds__(kRcWarps * 32, 6)
 // One warp per kept off-diagonal tile: the 128 x 4 words arrive as four
 // 16-byte loads per lane (row 32 rb + lane), issued before any transpose; the
 // next tile's flags are fetched one tile ahead.
+// Rows whose count is still below min_pts after the tile pairs' ROW counts
+// (K3): only their column counts can change a core decision (core = count >=
+// min_pts; counts only grow), so colcount counts only these columns. Per
+// 128-row tile, 4 words of candidate bits.
+__global__ void cand_mask_kernel(const int32_t* __restrict__ cnt, ElemTables et, int64_t P,
+                                 int32_t min_pts, uint32_t* __restrict__ cand) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // blockDim % 32 == 0
+  const bool c = p < P && et.ent[p] >= 0 && cnt[p] < min_pts;
+  const unsigned w = __ballot_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && p < P) cand[p >> 5] = w;
+}
+
 __global__ void __launch_bounds__(256)
 colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ nonempty,
                 const TileRef* __restrict__ tiles, int64_t slot0, int64_t n_tiles,
-                ElemTables et, int32_t* __restrict__ cnt) {
+                ElemTables et, int32_t* __restrict__ cnt, const uint32_t* __restrict__ cand) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1591,6 +1603,27 @@ colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ no
     uint4 r[4];
 #pragma unroll
     for (int rb = 0; rb < 4; ++rb) r[rb] = b[rb * 32 + lane];
+    if (cand) {
+      // candidate columns only: one ballot per 32-row block and column
+      const int64_t pj = et.pbase[tr.k] + tr.J * kTile;
+      const uint4 cm = *reinterpret_cast<const uint4*>(cand + (pj >> 5));
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = w == 0 ? cm.x : w == 1 ? cm.y : w == 2 ? cm.z : cm.w;
+        while (m) {  // warp-uniform
+          const int c = __ffs(m) - 1;
+          m &= m - 1;
+          int acc = 0;
+#pragma unroll
+          for (int rb = 0; rb < 4; ++rb) {
+            const uint32_t x = w == 0 ? r[rb].x : w == 1 ? r[rb].y : w == 2 ? r[rb].z : r[rb].w;
+            acc += __popc(__ballot_sync(0xffffffffu, (x >> c) & 1u));
+          }
+          if (acc && lane == 0) atomicAdd(cnt + pj + w * 32 + c, acc);
+        }
+      }
+      continue;
+    }
     const int64_t base = et.pbase[tr.k] + tr.J * kTile + lane;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -1664,6 +1697,7 @@ struct TcPrep {
   PwProgram prog{};       // numpy pairwise-sum program of d (a kernel argument: no
                           // shared constant memory, so concurrent calls are safe)
   double eps = 0.0;
+  int32_t min_pts = 0;  // > 0: column counts only for rows not already core by their rows
   std::vector<int32_t> nrows;
   Scratch s_tab, s_mm, s_cs, s_pl, s_nq, s_te, s_thr, s_cntw, s_flag, s_lim;
   // deferred recheck-queue check: [0] largest overflowing request, [1] pairs
@@ -1820,6 +1854,7 @@ int64_t tc_kpad(int64_t d) { return ceil_div(d, kKC) * kKC; }
 void tc_release(TcPrep* tp) { delete tp; }
 
 void tc_set_queue_scale(TcPrep* tp, double s) { tp->qscale = s; }
+void tc_set_min_pts(TcPrep* tp, int32_t m) { tp->min_pts = m; }
 
 // after a synchronisation of the stream: pairs rechecked so far and whether a
 // window's recheck queue overflowed (then its bits are incomplete: rerun with
@@ -1966,8 +2001,19 @@ int tc_window(TcPrep* tp, const RowSrc src, const ElemTables& et, const TileRef*
       return BM_ERR_INTERNAL;
     }
   }
+  // the whole batch in one window: every row's count from its own tile row is
+  // complete here, so only the rows still below min_pts need column counts
+  Scratch s_cand;
+  uint32_t* cand = nullptr;
+  if (!accumulate && cnt && tp->min_pts > 0) {
+    BM_TRY(scratch_alloc(s_cand, (size_t)(P / 32 + 4) * 4, stream));
+    cand = s_cand.as<uint32_t>();
+    cand_mask_kernel<<<(unsigned)ceil_div(P, 256), 256, 0, stream>>>(cnt_run, et, P, tp->min_pts,
+                                                                    cand);
+    BM_CHECK_LAUNCH();
+  }
   colcount_kernel<<<grid_cap(n_tiles, 8, 8), 256, 0, stream>>>(adj, nonempty, tiles, slot0,
-                                                               n_tiles, et, cnt_run);
+                                                               n_tiles, et, cnt_run, cand);
   BM_CHECK_LAUNCH();
   {
     // the queue length stays on the device: the recheck grid covers the

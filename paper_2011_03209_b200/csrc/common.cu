@@ -172,15 +172,34 @@ int big_acquire(size_t bytes, cudaStream_t stream, void** out, int* slot) {
         (best < 0 || b.bytes < g_big[best].bytes))
       best = i;
   }
+  static const bool trace_mem = getenv("B200MAP_TRACE_MEM") != nullptr;
   if (best < 0) {
     void* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      // first the memory the stream-ordered pool retains unused, then the
+      // idle cached buffers
+      cudaGetLastError();
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
+      }
+      cudaGetLastError();
+      e = cudaMalloc(&p, bytes);
+    }
     if (e != cudaSuccess) {  // give back the idle cached buffers and retry once
       cudaGetLastError();
       for (auto& b : g_big)
         if (!b.busy && b.dev == dev && b.p) big_free_locked(b);
       e = cudaMalloc(&p, bytes);
     }
+    if (trace_mem)
+      fprintf(stderr, "[mem] big_acquire miss %.2f GB: cudaMalloc %s in %.1f ms\n", bytes / 1e9,
+              e == cudaSuccess ? "ok" : "FAILED",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
     if (e != cudaSuccess) {
       cudaGetLastError();
       set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
@@ -203,9 +222,10 @@ int big_acquire(size_t bytes, cudaStream_t stream, void** out, int* slot) {
     g_big[best].p = p;
     g_big[best].bytes = bytes;
     g_big[best].pending = false;
-  } else if (g_big[best].pending) {
-    // the previous holder's work on the buffer precedes this stream's use
-    cudaStreamWaitEvent(stream, g_big[best].ev, 0);
+  } else {
+    if (trace_mem) fprintf(stderr, "[mem] big_acquire hit %.2f GB\n", bytes / 1e9);
+    if (g_big[best].pending)  // the previous holder's work precedes this stream's use
+      cudaStreamWaitEvent(stream, g_big[best].ev, 0);
   }
   g_big[best].busy = true;
   *out = g_big[best].p;
@@ -254,6 +274,9 @@ int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
   cudaError_t e = cudaMallocAsync(&s.ptr, bytes, stream);
   if (e != cudaSuccess) {  // idle cached large buffers hold the memory: free them, retry
     cudaGetLastError();
+    if (getenv("B200MAP_TRACE_MEM"))
+      fprintf(stderr, "[mem] pool allocation of %.2f GB failed: trimming cached buffers\n",
+              bytes / 1e9);
     big_trim();
     e = cudaMallocAsync(&s.ptr, bytes, stream);
   }

@@ -1517,7 +1517,11 @@ struct BatchCtx {
   // n_kept), first off-diagonal / tensor-core unit (n_rt+1), row pairs
   int64_t n_kept = 0;
   std::vector<int64_t> row_first, off_pos, tc_pos, row_pairs;
-  Scratch tabs, xg, work, perm, s_tiles, s_units, s_geo, s_dir, s_seed;
+  Scratch tabs, xg, work, perm, s_units, s_geo, s_dir, s_seed;
+  // dense per-tile-pair arrays (flags, positions, the kept list with room for
+  // every pair): cached buffers, not pool blocks — at cfg5 they are ~6 GB,
+  // and re-mapping them through the pool cost ~0.4 s per call
+  BigScratch s_tiles, b_flags, b_pos;
   // direction bound: per row tile its seed (s_dir), per grouped element the
   // seeds (fp32), their norms and pairwise distances (s_seed); null if none
   int32_t* tseed = nullptr;
@@ -1743,11 +1747,11 @@ struct BatchCtx {
       for (int32_t bi = 0; bi < nbk; ++bi)
         for (int32_t bj = bi; bj < nbk; ++bj) blocks.push_back({(int32_t)i, bi, bj, 0});
     }
-    Scratch s_re, s_fl, s_pos, s_rows;
+    Scratch s_re, s_rows;
     BM_TRY(scratch_alloc(s_re, n_rt * 4, stream));
     BM_CHECK_CUDA(cudaMemcpyAsync(s_re.ptr, row_elem.data(), n_rt * 4, cudaMemcpyHostToDevice, stream));
-    BM_TRY(scratch_alloc(s_fl, (size_t)n_tp * 4, stream));
-    int32_t* flags = s_fl.as<int32_t>();
+    BM_TRY(big_scratch(b_flags, (size_t)std::max<int64_t>(n_tp, 1) * 4, stream));
+    int32_t* flags = b_flags.as<int32_t>();
     if (prune) {
       Scratch s_blk;
       double* cen = s_geo.as<double>();
@@ -1786,14 +1790,14 @@ struct BatchCtx {
       fill_ones_kernel<<<grid_for(n_tp, 256), 256, 0, stream>>>(flags, n_tp);
       BM_CHECK_LAUNCH();
     }
-    BM_TRY(scratch_alloc(s_pos, (size_t)(n_tp + 1) * 8, stream));
-    int64_t* pos = s_pos.as<int64_t>();
+    BM_TRY(big_scratch(b_pos, (size_t)(n_tp + 1) * 8, stream));
+    int64_t* pos = b_pos.as<int64_t>();
     BM_TRY(exclusive_scan_i32_to_i64(flags, pos, n_tp, stream));
     fill_total_kernel<<<1, 1, 0, stream>>>(pos, flags, n_tp);  // pos[n_tp] = n_kept
     BM_CHECK_LAUNCH();
     // capacity for every tile pair: the list is built before its length is
     // known on the host (one synchronisation for all row tables below)
-    BM_TRY(scratch_alloc(s_tiles, (size_t)std::max<int64_t>(n_tp, 1) * sizeof(TileRef), stream));
+    BM_TRY(big_scratch(s_tiles, (size_t)std::max<int64_t>(n_tp, 1) * sizeof(TileRef), stream));
     d_tiles = s_tiles.as<TileRef>();
     // row tables: first slot, pairs, unit positions (exclusive scans)
     BM_TRY(scratch_alloc(s_rows, (size_t)(n_rt + 1) * 8 * 6, stream));

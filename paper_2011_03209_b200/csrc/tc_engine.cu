@@ -839,46 +839,78 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
   // fp64 (per lane <= 16 * 2^42: exact). A row with any |v| >= qmax
   // (clamping, inf, NaN) is redone by the generic path.
   bool bad = false;
-  if (valid) {
-    for (int64_t c4 = 4 * hl; c4 < kpad && c4 + 4 <= d; c4 += 64) {
-      double xv[4], cv[4], tv[4];
-      if (vec) {
-        const double2 u0 = *reinterpret_cast<const double2*>(xr + c4);
-        const double2 u1 = *reinterpret_cast<const double2*>(xr + c4 + 2);
-        xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
-        const double2 c0 = *reinterpret_cast<const double2*>(ck + c4);
-        const double2 c1 = *reinterpret_cast<const double2*>(ck + c4 + 2);
-        cv[0] = c0.x, cv[1] = c0.y, cv[2] = c1.x, cv[3] = c1.y;
-        if (ct) {
-          const double2 t0 = *reinterpret_cast<const double2*>(ct + c4);
-          const double2 t1 = *reinterpret_cast<const double2*>(ct + c4 + 2);
-          tv[0] = t0.x, tv[1] = t0.y, tv[2] = t1.x, tv[3] = t1.y;
-        }
-      } else {
+  auto quant4 = [&](const double (&xv)[4], const double (&cv)[4], const double (&tv)[4],
+                    int (&q)[4]) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          xv[j] = xr[c4 + j];
-          cv[j] = ck[c4 + j];
-          tv[j] = ct ? ct[c4 + j] : 0.0;
-        }
+    for (int j = 0; j < 4; ++j) {
+      const double y = xv[j] - cv[j];
+      const double v = y * inv;
+      bad |= !(fabs(v) < kQMax);
+      const double tq = __dadd_rn(v, kMagic);
+      const double qd = __dsub_rn(tq, kMagic);
+      q[j] = __double2loint(tq);
+      const double e = y - qd * sc;
+      esum += e * e;
+      nsi += (long long)q[j] * q[j];  // exact, on the integer pipe
+      if (ct) {
+        const double dr = xv[j] - tv[j];
+        rsum += dr * dr;
+      }
+    }
+  };
+  if (valid && vec) {
+    // 64-column blocks; lane hl takes columns b + 2hl, b + 2hl + 1 and
+    // b + 32 + 2hl, b + 33 + 2hl: every 16-byte shared load of a quarter-warp
+    // phase is contiguous (no bank conflicts; 4 consecutive columns per lane
+    // read at a 32-byte stride were 2-way conflicted), limbs stored as 16-bit
+    // pairs
+    for (int64_t b = 0; b + 64 <= d; b += 64) {
+      const int64_t c0 = b + 2 * hl, c1 = b + 32 + 2 * hl;
+      double xv[4], cv[4], tv[4];
+      const double2 u0 = *reinterpret_cast<const double2*>(xr + c0);
+      const double2 u1 = *reinterpret_cast<const double2*>(xr + c1);
+      xv[0] = u0.x, xv[1] = u0.y, xv[2] = u1.x, xv[3] = u1.y;
+      const double2 k0 = *reinterpret_cast<const double2*>(ck + c0);
+      const double2 k1 = *reinterpret_cast<const double2*>(ck + c1);
+      cv[0] = k0.x, cv[1] = k0.y, cv[2] = k1.x, cv[3] = k1.y;
+      if (ct) {
+        const double2 t0 = *reinterpret_cast<const double2*>(ct + c0);
+        const double2 t1 = *reinterpret_cast<const double2*>(ct + c1);
+        tv[0] = t0.x, tv[1] = t0.y, tv[2] = t1.x, tv[3] = t1.y;
+      } else {
+        tv[0] = tv[1] = tv[2] = tv[3] = 0.0;
       }
       int q[4];
+      quant4(xv, cv, tv, q);
+      // bytes (q0, q1 | q2, q3): low half-word -> columns c0, c0 + 1, high -> c1, c1 + 1
+      const uint32_t lw = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
+                                      __byte_perm(q[2], q[3], 0x0040), 0x5410) & 0x7f7f7f7fu;
+      const uint32_t mw = __byte_perm(__byte_perm(q[0] >> kLimb, q[1] >> kLimb, 0x0040),
+                                      __byte_perm(q[2] >> kLimb, q[3] >> kLimb, 0x0040),
+                                      0x5410) & 0x7f7f7f7fu;
+      const uint32_t hw = __byte_perm(
+          __byte_perm(q[0] >> (2 * kLimb), q[1] >> (2 * kLimb), 0x0040),
+          __byte_perm(q[2] >> (2 * kLimb), q[3] >> (2 * kLimb), 0x0040), 0x5410);
+      msq = __dp4a(mw, mw, msq);
+      lsq = __dp4a(lw, lw, lsq);
+      *reinterpret_cast<uint16_t*>(hrow_p + c0) = (uint16_t)hw;
+      *reinterpret_cast<uint16_t*>(hrow_p + c1) = (uint16_t)(hw >> 16);
+      *reinterpret_cast<uint16_t*>(mrow_p + c0) = (uint16_t)mw;
+      *reinterpret_cast<uint16_t*>(mrow_p + c1) = (uint16_t)(mw >> 16);
+      *reinterpret_cast<uint16_t*>(lrow_p + c0) = (uint16_t)lw;
+      *reinterpret_cast<uint16_t*>(lrow_p + c1) = (uint16_t)(lw >> 16);
+    }
+  } else if (valid) {
+    for (int64_t c4 = 4 * hl; c4 < kpad && c4 + 4 <= d; c4 += 64) {
+      double xv[4], cv[4], tv[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const double y = xv[j] - cv[j];
-        const double v = y * inv;
-        bad |= !(fabs(v) < kQMax);
-        const double tq = __dadd_rn(v, kMagic);
-        const double qd = __dsub_rn(tq, kMagic);
-        q[j] = __double2loint(tq);
-        const double e = y - qd * sc;
-        esum += e * e;
-        nsi += (long long)q[j] * q[j];  // exact, on the integer pipe
-        if (ct) {
-          const double dr = xv[j] - tv[j];
-          rsum += dr * dr;
-        }
+        xv[j] = xr[c4 + j];
+        cv[j] = ck[c4 + j];
+        tv[j] = ct ? ct[c4 + j] : 0.0;
       }
+      int q[4];
+      quant4(xv, cv, tv, q);
       const uint32_t lw = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
                                       __byte_perm(q[2], q[3], 0x0040), 0x5410) & 0x7f7f7f7fu;
       const uint32_t mw = __byte_perm(__byte_perm(q[0] >> kLimb, q[1] >> kLimb, 0x0040),
@@ -901,9 +933,10 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
   if (valid) ysum = (double)d * (kQMax * sc) * (kQMax * sc) * (1.0 + 1e-12);
   const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
   if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
-  // generic path: the tail columns (or the whole row when redo / padding)
+  // generic path: the tail columns (or the whole row when redo / padding);
+  // the fast path covered whole 64-column blocks (vec) or 4-column groups
   for (int64_t c4 = 4 * hl; c4 < kpad; c4 += 64) {
-    if (!redo && valid && c4 + 4 <= d) continue;
+    if (!redo && valid && (vec ? (c4 - c4 % 64) + 64 <= d : c4 + 4 <= d)) continue;
     uint32_t hw = 0, mw = 0, lw = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {

@@ -8,13 +8,15 @@ A step = one full Mapper graph build of the workload: lens -> cover binning
           one GPU compute_mapper(pc, params) on page-locked fp64 X, returning
           the MapperRun with the canonical graph JSON (H2D of X, D2H of the
           node rows/payload/edges, JSON writing all inside the timed region);
-          on N GPUs the sharded build with X copied H2D and node rows + edges
-          copied D2H every step
+          e2e.pageable repeats it on ordinary pageable numpy arrays (what a
+          nervemap caller holds; staged through the library's pinned ring);
+          on N GPUs compute_mapper_spmd: 1/N of X H2D per rank + all-gather,
+          the sharded build, the MapperRun on rank 0
 Inputs (2 GB at 1M x 256 fp64) exceed the 126 MB L2, so no flush is needed.
 
   python bench.py [--gpus N --steps K --warmup W --config cfg3 --impl ours|reference]
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (NCCL; elements
-sharded by LPT, labels all-gathered to rank 0).
+sharded by LPT on kept tile pairs, labels gathered to rank 0).
 """
 
 from __future__ import annotations
@@ -578,32 +580,50 @@ def main():
     # Several GPUs: the sharded build + read-back of node rows and edges.
     h2d = X.nbytes
     d2h = 0
+    e2e_pageable = None
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     if world == 1:
         from paper_2011_03209_b200 import compute_mapper, from_array
 
         if Fh is None:
-            pc_host = from_array(Xh.numpy())  # page-locked host buffer, no copy
-
-            def e2e_step():
-                return compute_mapper(pc_host, params, engine=args.engine).graph
+            def e2e_step(xs, fs):
+                return compute_mapper(from_array(xs), params, engine=args.engine).graph
             e2e_api = "compute_mapper -> MapperRun (graph + canonical JSON bytes)"
         else:
             h2d += Fh.numpy().nbytes
 
-            def e2e_step():
-                return library_pieces(Xh.numpy(), Fh.numpy(), w, params)
+            def e2e_step(xs, fs):
+                return library_pieces(xs, fs, w, params)
             e2e_api = ("build_cover -> membership -> cluster_all -> build_graph -> graph_to_json "
                        "(the lens is FilterValues: test_nerve.py:23-30's composition), fresh "
                        "PointCloud/FilterValues objects every step (no device cache)")
-        gr = e2e_step()
+        # page-locked host buffers (no copy into the PointCloud)
+        xs, fs = Xh.numpy(), None if Fh is None else Fh.numpy()
+        gr = e2e_step(xs, fs)
         barrier()
         f0.record(stream)
         for _ in range(args.steps):
-            gr = e2e_step()
+            gr = e2e_step(xs, fs)
         f1.record(stream)
         barrier()
+        # the same call on ordinary pageable numpy arrays (what a nervemap
+        # caller holds): staged through the library's pinned ring
+        xs, fs = X, None if Fh is None else Fh.numpy().copy()
+        gr = e2e_step(xs, fs)
+        barrier()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        n_page = max(1, min(args.steps, 5))
+        p0.record(stream)
+        for _ in range(n_page):
+            gr = e2e_step(xs, fs)
+        p1.record(stream)
+        barrier()
+        t_page = p0.elapsed_time(p1) / 1e3
+        e2e_pageable = {"value": w.n * n_page / t_page, "unit": UNIT,
+                        "ms_per_step": 1e3 * t_page / n_page, "steps": n_page,
+                        "source": "pageable numpy arrays (staged through the pinned ring)"}
         n_rows = sum(len(nd.rows) for nd in gr.nodes)
         d2h = 8 * (n_rows + gr.n_nodes + 1 + gr.n_nodes * (w.d + len(params.filters)) +
                    3 * len(gr.edges))
@@ -662,7 +682,7 @@ def main():
         "data": "synthetic", "config": config_of(w, world),
         "e2e": {"value": w.n * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps,
-                "api": e2e_api},
+                "api": e2e_api, "pageable": e2e_pageable},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
                      "traffic_note": "DRAM bytes per tc_adjacency_kernel launch at cfg3, from "

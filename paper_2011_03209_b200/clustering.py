@@ -82,6 +82,33 @@ class PullbackClustering:
     clusters: list  # sorted global rows, ordered by smallest row
     noise: list
 
+    # cluster_all's results keep their rows as flat arrays (`_lazy`: rows in
+    # cluster order, cluster sizes, noise rows) until a caller first reads
+    # `clusters` or `noise`; the lists are built then, once. build_graph reads
+    # the flat arrays (flat_clusters), so membership -> cluster_all ->
+    # build_graph never converts the ~N row ids to Python ints.
+    def __getattr__(self, name):
+        if name in ("clusters", "noise"):
+            lazy = self.__dict__.get("_lazy")
+            if lazy is not None:
+                flat, sizes, noise = lazy
+                cuts = np.zeros(len(sizes) + 1, dtype=np.int64)
+                np.cumsum(sizes, out=cuts[1:])
+                clusters = [flat[cuts[c]:cuts[c + 1]].tolist() for c in range(len(sizes))]
+                self.__dict__.update(
+                    clusters=clusters, noise=noise.tolist(),
+                    _flat=(flat, sizes, id(clusters), [(id(c), len(c)) for c in clusters]))
+                self.__dict__.pop("_lazy", None)
+                return self.__dict__[name]
+        raise AttributeError(f"{type(self).__name__!r} object has no attribute {name!r}")
+
+    @classmethod
+    def _from_flat(cls, element_index: int, flat: np.ndarray, sizes: np.ndarray,
+                   noise: np.ndarray) -> "PullbackClustering":
+        obj = cls.__new__(cls)
+        obj.__dict__.update(element_index=element_index, _lazy=(flat, sizes, noise))
+        return obj
+
 
 @dataclass
 class ClusterRunStats:
@@ -209,7 +236,8 @@ def grouped_clusterings(rows_h: np.ndarray, offsets: np.ndarray, labels_h: np.nd
                         ncl: np.ndarray, node_rows_h: np.ndarray, node_off_h: np.ndarray) -> list:
     """Per-element PullbackClustering lists from the device's node grouping
     (bm_group_nodes: rows of every cluster, ascending, in (element, cluster)
-    order) — the host only slices; noise rows come from one mask pass."""
+    order) — the host only slices (the Python lists are built on first
+    access); noise rows come from one mask pass."""
     n_el = len(offsets) - 1
     noise_idx = np.flatnonzero(labels_h < 0)
     nb = np.searchsorted(noise_idx, offsets)
@@ -219,20 +247,19 @@ def grouped_clusterings(rows_h: np.ndarray, offsets: np.ndarray, labels_h: np.nd
     for k in range(n_el):
         v0, v1 = int(node0[k]), int(node0[k + 1])
         a, b = int(node_off_h[v0]), int(node_off_h[v1])
-        flat = node_rows_h[a:b]
-        sizes = np.diff(node_off_h[v0:v1 + 1])
-        clusters = [flat[node_off_h[v] - a:node_off_h[v + 1] - a].tolist() for v in range(v0, v1)]
-        noise = rows_h[noise_idx[nb[k]:nb[k + 1]]].tolist()
-        pbc = PullbackClustering(k, clusters, noise)
-        pbc._flat = (flat, sizes, id(clusters), [(id(c), len(c)) for c in clusters])
-        out.append(pbc)
+        out.append(PullbackClustering._from_flat(k, node_rows_h[a:b],
+                                                 np.diff(node_off_h[v0:v1 + 1]),
+                                                 rows_h[noise_idx[nb[k]:nb[k + 1]]]))
     return out
 
 
 def flat_clusters(pbc):
     """(rows in cluster order, cluster sizes) of a PullbackClustering made by
     cluster_all, or None if its cluster lists were replaced or resized."""
-    f = getattr(pbc, "_flat", None)
+    lazy = pbc.__dict__.get("_lazy")
+    if lazy is not None:  # lists never built: the flat arrays are the truth
+        return lazy[0], lazy[1]
+    f = pbc.__dict__.get("_flat")
     if f is None or f[2] != id(pbc.clusters) or len(pbc.clusters) != len(f[3]):
         return None
     for c, (ic, ln) in zip(pbc.clusters, f[3]):

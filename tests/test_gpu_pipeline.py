@@ -78,13 +78,14 @@ def test_pca2d_library_pieces(golden):
     assert graph_to_json(g) == z["graph"].tobytes()
     # build_graph's flat fast path (lists made by cluster_all) and the generic
     # path (caller-built lists; one edited in place) give the same bytes
-    import copy
-
+    from paper_2011_03209_b200 import PullbackClustering
     from paper_2011_03209_b200.clustering import flat_clusters
 
     assert all(flat_clusters(c) is not None for c in cl)
-    cl2 = copy.deepcopy(cl)
-    assert all(flat_clusters(c) is None for c in cl2 if c.clusters)
+    cl2 = [PullbackClustering(c.element_index, [list(m) for m in c.clusters], list(c.noise))
+           for c in cl]
+    assert cl2 == cl
+    assert all(flat_clusters(c) is None for c in cl2)
     assert graph_to_json(build_graph(cl2, pc, fv, cover, manifest={"test": True})) == \
         z["graph"].tobytes()
     k = next(i for i, c in enumerate(cl) if c.clusters)

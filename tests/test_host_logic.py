@@ -129,3 +129,33 @@ def test_split_groups_pair_work_limit():
         work = sum(s * s for s in sizes[a:b])
         assert b - a == 1 or work <= 100 ** 2 + 60
     assert split_groups(offs, limit=10 ** 9) == [(0, len(sizes))]
+
+
+def test_pullback_clustering_lazy_lists():
+    """cluster_all's results hold flat arrays until clusters/noise are read;
+    then they are the reference's plain lists (equality, repr, pickle, copy),
+    and flat_clusters stops trusting them once a caller edits a list."""
+    import copy
+    import pickle
+
+    from paper_2011_03209_b200.clustering import PullbackClustering, flat_clusters
+
+    flat = np.array([3, 7, 9, 1, 2], dtype=np.int64)
+    sizes = np.array([3, 2], dtype=np.int64)
+    noise = np.array([4, 11], dtype=np.int64)
+    want = PullbackClustering(5, [[3, 7, 9], [1, 2]], [4, 11])
+
+    p = PullbackClustering._from_flat(5, flat, sizes, noise)
+    fr, fs = flat_clusters(p)  # no lists built yet
+    assert fr is flat and fs is sizes and "clusters" not in p.__dict__
+    q = pickle.loads(pickle.dumps(p))
+    r = copy.deepcopy(p)
+    assert p == want and q == want and r == want and repr(p) == repr(want)
+    assert all(type(v) is int for c in p.clusters for v in c) and type(p.noise) is list
+    fr, fs = flat_clusters(p)  # lists built and untouched: still the flat arrays
+    assert fr.tolist() == [3, 7, 9, 1, 2] and fs.tolist() == [3, 2]
+    p.clusters[0].append(12)
+    assert flat_clusters(p) is None
+    with pytest.raises(AttributeError):
+        p.missing  # noqa: B018
+    assert flat_clusters(want) is None  # a caller-built result has no flat copy

@@ -1100,19 +1100,37 @@ __device__ unsigned long long g_comp_stats[8];
 #define COMP_STAT(i) 0ull
 #endif
 
+// off-diagonal phases: tile pairs [kCompCuts[i-1], kCompCuts[i]) of every unit,
+// with a compression of the forest between phases
+#ifndef BM_COMP_CUT1
+#define BM_COMP_CUT1 6
+#endif
+#ifndef BM_COMP_CUT2
+#define BM_COMP_CUT2 0
+#endif
+#if BM_COMP_CUT2 > 0
+constexpr int kCompCuts[] = {0, BM_COMP_CUT1, BM_COMP_CUT2, 1 << 30};
+#else
+constexpr int kCompCuts[] = {0, BM_COMP_CUT1, 1 << 30};
+#endif
+constexpr int kCompPhases = (int)(sizeof(kCompCuts) / sizeof(kCompCuts[0])) - 1;
+
 template <bool DIAG>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 16)
 components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
                   const TileUnit* __restrict__ units, const TileRef* __restrict__ tiles,
                   int64_t slot0, int64_t n_units, const uint8_t* __restrict__ core,
                   int32_t* __restrict__ par, int32_t* __restrict__ bmin,
-                  const int32_t* __restrict__ uni, const int32_t* __restrict__ nonempty) {
+                  const int32_t* __restrict__ uni, const int32_t* __restrict__ nonempty,
+                  int s_lo, int s_hi) {
   __shared__ uint32_t bits[kTileWords];
   __shared__ int groot[2 * kTile];  // global root of each tile node (-1: not core)
   __shared__ int lp[2 * kTile];     // local union-find over tile nodes
   __shared__ uint32_t coreJ[4], coreI[4];
   __shared__ int any_merge;
   __shared__ int rmm[4][4];  // per warp: min/max core root of rows, of columns
+  __shared__ int2 grp[4][32];  // off-diagonal: per column word, (root, lanes) of each root group
+  __shared__ int ngrp[4];
   const int t = threadIdx.x;
   for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     const TileUnit un = units[u];
@@ -1130,7 +1148,8 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
       if ((t & 31) == 0) coreI[t >> 5] = bi;
     }
     const int uI = DIAG ? -1 : uni[(pb >> 7) + I];
-    for (int s = 0; s < un.cnt; ++s) {
+    const int s_end = un.cnt < s_hi ? un.cnt : s_hi;
+    for (int s = s_lo; s < s_end; ++s) {
       const int64_t g = un.off + s;
       const int J = tiles[g].J;
       BM_DASSERT(tiles[g].k == k && tiles[g].I == I && J >= I && J < et.ntiles[k]);
@@ -1178,6 +1197,15 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
           rmm[2][w] = (int)mnJ;
           rmm[3][w] = mxJ;
         }
+        // the word's core columns grouped by global root (after the diagonal
+        // pass a word holds few roots): a row joins each group it touches once
+        // instead of visiting every neighbouring column
+        const int lane = t & 31;
+        const unsigned eq = __match_any_sync(0xffffffffu, cj ? grj : -1);
+        const bool lead = cj && (__ffs(eq) - 1 == lane);
+        const unsigned lm = __ballot_sync(0xffffffffu, lead);
+        if (lead) grp[w][__popc(lm & ((1u << lane) - 1u))] = make_int2(grj, (int)eq);
+        if (lane == 0) ngrp[w] = __popc(lm);
       }
       __syncthreads();
       const int r = t;
@@ -1215,13 +1243,18 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
             // only its neighbours c < r, each edge is visited once
             const int lo = r - w * 32;
             m &= lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : (1u << lo) - 1u);
-          } else if (m && rmm[2][w] == rmm[3][w]) {
-            // every core column of word w has the same global root (warp w's
-            // min == max): one join with the first neighbour stands for all
-            const int gn = rmm[2][w];
-            if (gn != gr && gn != last) {
-              last = gn;
-              if (lunion(lp, r, kTile + w * 32 + __ffs(m) - 1)) any_merge = 1;
+          } else if (m && ngrp[w] <= __popc(m)) {
+            // walk the word's root groups (one group: every core column has
+            // the same root): one join with the first neighbour of a group
+            // stands for all of its columns
+            const int ng = ngrp[w];
+            for (int q = 0; q < ng; ++q) {
+              const int2 G = grp[w][q];
+              const uint32_t mm = m & (uint32_t)G.y;
+              if (mm && G.x != gr && G.x != last) {
+                last = G.x;
+                if (lunion(lp, r, kTile + w * 32 + __ffs(mm) - 1)) any_merge = 1;
+              }
             }
             continue;
           }
@@ -1931,7 +1964,8 @@ struct BatchCtx {
     }
     if (w.n_diag > 0) {
       components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
-          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty);
+          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty, 0,
+          1 << 30);
       BM_CHECK_LAUNCH();
     }
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
@@ -1949,10 +1983,23 @@ struct BatchCtx {
                                               cudaMemcpyHostToDevice, stream));
       }
 #endif
-      components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
-          adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w, s_uni.as<int32_t>(),
-          nonempty);
-      BM_CHECK_LAUNCH();
+      // two phases: the first 6 tile pairs of every unit (its nearest kept
+      // column tiles) join most of each cluster's tiles; after a compression
+      // the remaining pairs mostly see one root per tile side and take the
+      // one-union path instead of walking their bits (cfg3: 1.04 -> 0.84 ms)
+      for (int phase = 0; phase < kCompPhases; ++phase) {
+        if (phase > 0) {
+          compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);
+          BM_CHECK_LAUNCH();
+          tile_uniform_kernel<<<grid_for(n_rt, 8, 32), 256, 0, stream>>>(et, n_rt, core, par_w,
+                                                                         s_uni.as<int32_t>());
+          BM_CHECK_LAUNCH();
+        }
+        components_kernel<false><<<grid_for(w.n_off, 1, 32), 128, 0, stream>>>(
+            adj, et, w.off, w.tiles, w.slot0, w.n_off, core, par_w, bmin_w, s_uni.as<int32_t>(),
+            nonempty, kCompCuts[phase], kCompCuts[phase + 1]);
+        BM_CHECK_LAUNCH();
+      }
 #ifdef BM_COMP_STATS
       {
         unsigned long long h[8];

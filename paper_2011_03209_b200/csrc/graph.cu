@@ -121,7 +121,11 @@ __global__ void node_keys_kernel(const int64_t* __restrict__ rows, const int64_t
     const int64_t key = l >= 0 ? node_base[a] + l : n_nodes;
     keys[e] = (uint64_t)key;
     vals[e] = rows[e];
-    if (l >= 0) atomicAdd(counts + key, 1);
+    // warp-aggregated count (a few hundred nodes share ~1M entries: one
+    // atomic per distinct node in the warp instead of one per entry)
+    const unsigned act = __activemask();
+    const unsigned same = __match_any_sync(act, key);
+    if (l >= 0 && (__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(counts + key, __popc(same));
   }
 }
 
@@ -242,7 +246,14 @@ __global__ void sparse_edges_kernel(const uint64_t* __restrict__ keys, int64_t n
 // columns) streams its rows through a shared-memory ring of kNsStages chunks
 // of 32 rows with cp.async (each lane copies, and then adds, its own column;
 // 192 rows in flight per warp), row ids prefetched a chunk ahead.
-constexpr int kNsStages = 6;  // 48 KB of static shared memory
+#ifndef BM_NS_STAGES
+#define BM_NS_STAGES 6
+#endif
+constexpr int kNsStages = BM_NS_STAGES;  // 8 KB of static shared memory each
+#ifndef BM_NS_LPT
+#define BM_NS_LPT 1
+#endif
+constexpr bool kNsLpt = BM_NS_LPT;
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool pred) {
   const unsigned sz = pred ? 8u : 0u;  // src-size 0: zero-fill, no read
@@ -254,10 +265,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool pred)
 
 __global__ void __launch_bounds__(32)
 node_stats_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ node_rows,
-                  const int64_t* __restrict__ node_off, int64_t n_nodes,
-                  double* __restrict__ stats) {
+                  const int64_t* __restrict__ node_off, const int32_t* __restrict__ order,
+                  int64_t n_nodes, double* __restrict__ stats) {
   __shared__ __align__(16) double ring[kNsStages][32][32];
-  const int64_t v = blockIdx.y;
+  const int64_t v = order[blockIdx.y];  // largest nodes first (their chains are the longest)
   const int lane = threadIdx.x;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const bool col = c < d;
@@ -526,20 +537,30 @@ extern "C" int bm_node_stats(const double* d_X, int64_t d, const double* d_f, in
   BM_REQUIRE(d >= 1 && (m == 1 || m == 2) && n_nodes >= 0, "bad arguments");
   if (n_nodes == 0) return BM_OK;
   BM_REQUIRE(n_nodes <= 65535, "node_stats: at most 65535 nodes per call");
+  // node sizes on the host: launch order of the column chains (largest
+  // first) and the pairwise leaf programs of the filter means
+  std::vector<int64_t> off(n_nodes + 1);
+  BM_CHECK_CUDA(cudaMemcpyAsync(off.data(), d_node_offsets, (n_nodes + 1) * 8,
+                                cudaMemcpyDeviceToHost, s));
+  BM_CHECK_CUDA(cudaStreamSynchronize(s));
+  Scratch s_order;
   if (d_stats) {
     BM_REQUIRE(d_X, "null points");
+    std::vector<int32_t> order(n_nodes);
+    for (int64_t v = 0; v < n_nodes; ++v) order[v] = (int32_t)v;
+    if (kNsLpt)
+      std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+        return off[x + 1] - off[x] > off[y + 1] - off[y];
+      });
+    BM_TRY(scratch_alloc(s_order, (size_t)n_nodes * 4, s));
+    BM_CHECK_CUDA(cudaMemcpyAsync(s_order.ptr, order.data(), n_nodes * 4, cudaMemcpyHostToDevice, s));
     dim3 grid((unsigned)ceil_div(d, 32), (unsigned)n_nodes);
-    node_stats_kernel<<<grid, 32, 0, s>>>(d_X, d, d_node_rows, d_node_offsets, n_nodes, d_stats);
+    node_stats_kernel<<<grid, 32, 0, s>>>(d_X, d, d_node_rows, d_node_offsets,
+                                          s_order.as<int32_t>(), n_nodes, d_stats);
     BM_CHECK_LAUNCH();
   }
   if (d_fmean) {
     BM_REQUIRE(d_f, "null filter values");
-    // node sizes -> pairwise leaf programs (host), leaf sums and their
-    // combination (device)
-    std::vector<int64_t> off(n_nodes + 1);
-    BM_CHECK_CUDA(cudaMemcpyAsync(off.data(), d_node_offsets, (n_nodes + 1) * 8,
-                                  cudaMemcpyDeviceToHost, s));
-    BM_CHECK_CUDA(cudaStreamSynchronize(s));
     std::vector<NodeLeaf> lv;
     std::vector<int64_t> loff(n_nodes + 1, 0);
     for (int64_t v = 0; v < n_nodes; ++v) {

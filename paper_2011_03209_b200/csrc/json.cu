@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <charconv>
 #include <thread>
 #include <vector>
 
@@ -83,7 +84,9 @@ struct Out {
   bool put_num(double v) {
     if (!(v == v) || v == __builtin_inf() || v == -__builtin_inf()) return false;
     char t[40];
-    const int n = snprintf(t, sizeof t, "%.9g", v);
+    // std::to_chars with a precision is specified as printf's "%.*g" in the
+    // C locale (correctly rounded), ~4x faster than snprintf
+    const int n = (int)(std::to_chars(t, t + sizeof t, v, std::chars_format::general, 9).ptr - t);
     if (n == 2 && t[0] == '-' && t[1] == '0') {
       put("0", 1);
     } else {
@@ -212,12 +215,16 @@ extern "C" int bm_json_nodes(int64_t n_nodes, const int64_t* h_node_rows,
       give_back(cache.parts);
       cache.valid = false;
     }
-    const int64_t total = n_nodes ? h_node_off[n_nodes] : 0;
+    // cost of node v ~ its row ids + kNumCost per formatted number (one
+    // "%.9g" costs about as much as 30 row ids)
+    constexpr int64_t kNumCost = 30;
+    auto work = [&](int64_t v) { return h_node_off[v] + v * (d + m) * kNumCost; };
+    const int64_t total = n_nodes ? work(n_nodes) : 0;
     const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, total / 32768));
     std::vector<int64_t> cut(nt + 1, n_nodes);
     cut[0] = 0;
     for (int t = 1, v = 0; t < nt; ++t) {
-      while (v < n_nodes && h_node_off[v] < total * t / nt) ++v;
+      while (v < n_nodes && work(v) < total * t / nt) ++v;
       cut[t] = v;
     }
     parts.resize(nt);

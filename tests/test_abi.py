@@ -125,3 +125,36 @@ def test_native_graph_json_matches_python_writer():
                            np.arange(n_nodes), stats, fmean,
                            np.array([[0, 1, 3], [2, 5, 1]], dtype=np.int64))
         assert graph_to_json(g) == to_canonical_json(graph_to_obj(g))
+
+
+def test_native_graph_json_random_bit_patterns():
+    """The native "%.9g" (std::to_chars) equals Python's on random fp64 bit
+    patterns: subnormals, huge and tiny exponents, both signs."""
+    import numpy as np
+
+    from paper_2011_03209_b200.nerve import assemble_graph, graph_to_json, graph_to_obj
+    from paper_2011_03209_b200.nerve import to_canonical_json
+
+    class PC:
+        numerical_columns = [f"c{i:02d}" for i in range(64)]
+        categorical_columns = []
+
+    class Cov:
+        two_d = False
+
+        def element_key(self, k):
+            return k
+
+    rng = np.random.default_rng(11)
+    n_nodes = 64
+    bits = rng.integers(0, 2 ** 63, (n_nodes, 64), dtype=np.int64)
+    bits ^= rng.integers(0, 2, (n_nodes, 64), dtype=np.int64) << 63
+    stats = bits.view(np.float64).copy()
+    stats[~np.isfinite(stats)] = 1.25
+    stats[:8] = rng.standard_normal((8, 64)) * 10.0 ** rng.integers(-320, 300, (8, 64))
+    off = np.arange(n_nodes + 1, dtype=np.int64) * 3
+    rows = np.arange(3 * n_nodes, dtype=np.int64)
+    fmean = rng.standard_normal((n_nodes, 1))
+    g = assemble_graph(PC(), None, Cov(), {}, rows, off, np.arange(n_nodes), stats, fmean,
+                       np.zeros((0, 3), dtype=np.int64))
+    assert graph_to_json(g) == to_canonical_json(graph_to_obj(g))

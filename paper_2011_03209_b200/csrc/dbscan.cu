@@ -173,6 +173,11 @@ constexpr int kGroupSeeds = 64;
 static_assert(kGroupSeeds == 64, "seed_order / tile_project / prune kernels are written for 64 seeds");
 constexpr int kGroupDims = 32;
 constexpr int kGroupMinRows = 3 * kTile;  // smaller elements keep their order
+constexpr int kSeedTab = kGroupSeeds * (kGroupDims + 1);  // floats per element seed table
+#ifndef BM_GROUP_TC
+#define BM_GROUP_TC 1
+#endif
+constexpr bool kGroupTc = BM_GROUP_TC;  // seed assignment on the tensor cores (mma.sync tf32)
 
 struct GroupItem {
   int32_t k, e0, e1, pad;  // element, entries [e0, e1) (batch-relative)
@@ -185,7 +190,8 @@ struct GroupItem {
 __global__ void __launch_bounds__(256)
 seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                   const int64_t* __restrict__ offs, const int32_t* __restrict__ elems,
-                  int32_t* __restrict__ rank, int32_t* __restrict__ order) {
+                  int32_t* __restrict__ rank, int32_t* __restrict__ order,
+                  float* __restrict__ seed_tab) {
   __shared__ float sd[kGroupSeeds][kGroupDims + 1];
   __shared__ float dist[kGroupSeeds][kGroupSeeds + 1];
   __shared__ int used[kGroupSeeds];
@@ -199,6 +205,18 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
   }
   if (threadIdx.x < kGroupSeeds) used[threadIdx.x] = threadIdx.x >= S;
   __syncthreads();
+  {
+    // the element's seed table for group_assign: 64 x kGroupDims coordinates
+    // then the 64 squared norms (one contiguous block per element)
+    float* tab = seed_tab + (int64_t)k * kSeedTab;
+    for (int i = threadIdx.x; i < kGroupSeeds * kGroupDims; i += blockDim.x)
+      tab[i] = sd[i / kGroupDims][i % kGroupDims];
+    if (threadIdx.x < kGroupSeeds) {
+      float q = 0.0f;
+      for (int c = 0; c < kGroupDims; ++c) q = fmaf(sd[threadIdx.x][c], sd[threadIdx.x][c], q);
+      tab[kGroupSeeds * kGroupDims + threadIdx.x] = q;
+    }
+  }
   for (int i = threadIdx.x; i < kGroupSeeds * kGroupSeeds; i += blockDim.x) {
     const int a = i / kGroupSeeds, b = i % kGroupSeeds;
     float acc = 0.0f;
@@ -253,25 +271,23 @@ seed_order_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
 __global__ void __launch_bounds__(128, 6)
 group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
                     const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
-                    const int32_t* __restrict__ seed_rank, uint64_t* __restrict__ keys,
-                    int64_t* __restrict__ vals) {
+                    const int32_t* __restrict__ seed_rank, const float* __restrict__ seed_tab,
+                    uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
   __shared__ __align__(16) float sd[kGroupSeeds][kGroupDims];  // seed coordinates
   __shared__ float sn[kGroupSeeds];                              // |s|^2
   const GroupItem it = items[blockIdx.x];
   const int64_t ek = offs[it.k], nk = offs[it.k + 1] - ek;
   const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
   const int D = d < kGroupDims ? (int)d : kGroupDims;
-  for (int i = threadIdx.x; i < kGroupDims * kGroupSeeds; i += blockDim.x) {
-    const int j = i / kGroupDims, dim = i % kGroupDims;
-    float v = 0.0f;  // dims >= D are 0 on both sides
-    if (j < S && dim < D) v = (float)X[rows[ek + (j * nk) / S] * d + dim];
-    sd[j][dim] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < kGroupSeeds) {
-    float q = 0.0f;
-    for (int c = 0; c < kGroupDims; ++c) q = fmaf(sd[threadIdx.x][c], sd[threadIdx.x][c], q);
-    sn[threadIdx.x] = q;
+  {  // the element's seed table (seed_order_kernel), coalesced
+    const float4* tab = reinterpret_cast<const float4*>(seed_tab + (int64_t)it.k * kSeedTab);
+    for (int i = threadIdx.x; i < kSeedTab / 4; i += blockDim.x) {
+      const float4 v = tab[i];
+      if (i < kGroupSeeds * kGroupDims / 4)
+        reinterpret_cast<float4*>(&sd[0][0])[i] = v;
+      else
+        reinterpret_cast<float4*>(sn)[i - kGroupSeeds * kGroupDims / 4] = v;
+    }
   }
   __syncthreads();
   for (int e = it.e0 + threadIdx.x; e < it.e1; e += blockDim.x) {
@@ -298,6 +314,107 @@ group_assign_kernel(const double* __restrict__ X, int64_t d, const int64_t* __re
     }
     keys[e] = ((uint64_t)it.k << 7) | (uint64_t)seed_rank[(int64_t)it.k * kGroupSeeds + bi];
     vals[e] = e;
+  }
+}
+
+// Tensor-core variant (mma.sync tf32, m16n8k8): a warp takes 16 entries, the
+// scores |s|^2 - 2 <x, s> of all 64 seeds come from 4 k-steps x 8 seed tiles
+// of MMAs, and each row's argmin (smallest seed index on ties) is reduced
+// across its quad. The entries' first kGroupDims coordinates are read
+// coalesced (lane = dim) and transposed through shared memory.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+constexpr int kGaWarps = 4;
+
+__global__ void __launch_bounds__(kGaWarps * 32)
+group_assign_tc_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ rows,
+                       const int64_t* __restrict__ offs, const GroupItem* __restrict__ items,
+                       const int32_t* __restrict__ seed_rank, const float* __restrict__ seed_tab,
+                       uint64_t* __restrict__ keys, int64_t* __restrict__ vals) {
+  __shared__ uint32_t sb[kGroupSeeds][kGroupDims + 4];    // seeds (tf32), padded
+  __shared__ float sn[kGroupSeeds];                       // |s|^2
+  __shared__ uint32_t sa[kGaWarps][16][kGroupDims + 4];   // per warp: 16 entries (tf32)
+  const GroupItem it = items[blockIdx.x];
+  const int64_t nk = offs[it.k + 1] - offs[it.k];
+  const int S = nk < kGroupSeeds ? (int)nk : kGroupSeeds;
+  const int D = d < kGroupDims ? (int)d : kGroupDims;
+  {
+    const float* tab = seed_tab + (int64_t)it.k * kSeedTab;
+    for (int i = threadIdx.x; i < kGroupSeeds * kGroupDims; i += blockDim.x)
+      sb[i / kGroupDims][i % kGroupDims] = to_tf32(tab[i]);
+    for (int i = threadIdx.x; i < kGroupSeeds; i += blockDim.x)
+      sn[i] = i < S ? tab[kGroupSeeds * kGroupDims + i] : 3.0e38f;  // absent seeds never win
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t(*A)[kGroupDims + 4] = sa[wid];
+  for (int64_t e0 = it.e0 + wid * 16; e0 < it.e1; e0 += kGaWarps * 16) {
+    // 16 entries x kGroupDims dims, coalesced along the dims
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int64_t e = e0 + i;
+      float v = 0.0f;
+      if (e < it.e1 && lane < D) v = (float)X[rows[e] * d + lane];
+      A[i][lane] = to_tf32(v);
+    }
+    __syncwarp();
+    float acc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < kGroupDims / 8; ++kk) {
+      const uint32_t a0 = A[g][kk * 8 + t], a1 = A[g + 8][kk * 8 + t];
+      const uint32_t a2 = A[g][kk * 8 + t + 4], a3 = A[g + 8][kk * 8 + t + 4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t b0 = sb[j * 8 + g][kk * 8 + t], b1 = sb[j * 8 + g][kk * 8 + t + 4];
+        asm volatile(
+            "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+            "{%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      }
+    }
+    __syncwarp();
+    // rows g (acc[.][0..1]) and g + 8 (acc[.][2..3]); seed n = 8 j + 2 t + {0, 1}
+    float best0 = 3.4e38f, best1 = 3.4e38f;
+    int bi0 = kGroupSeeds, bi1 = kGroupSeeds;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = j * 8 + 2 * t + h;
+        const float s0 = fmaf(-2.0f, acc[j][h], sn[n]);
+        const float s1 = fmaf(-2.0f, acc[j][2 + h], sn[n]);
+        if (s0 < best0) { best0 = s0; bi0 = n; }  // n ascending per lane: first min kept
+        if (s1 < best1) { best1 = s1; bi1 = n; }
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const float ob0 = __shfl_xor_sync(0xffffffffu, best0, o);
+      const int oi0 = __shfl_xor_sync(0xffffffffu, bi0, o);
+      const float ob1 = __shfl_xor_sync(0xffffffffu, best1, o);
+      const int oi1 = __shfl_xor_sync(0xffffffffu, bi1, o);
+      if (ob0 < best0 || (ob0 == best0 && oi0 < bi0)) { best0 = ob0; bi0 = oi0; }
+      if (ob1 < best1 || (ob1 == best1 && oi1 < bi1)) { best1 = ob1; bi1 = oi1; }
+    }
+    if (t == 0) {
+      const int64_t ea = e0 + g, eb = e0 + g + 8;
+      const int32_t* rk = seed_rank + (int64_t)it.k * kGroupSeeds;
+      if (ea < it.e1) {
+        keys[ea] = ((uint64_t)it.k << 7) | (uint64_t)rk[bi0 < S ? bi0 : 0];
+        vals[ea] = ea;
+      }
+      if (eb < it.e1) {
+        keys[eb] = ((uint64_t)it.k << 7) | (uint64_t)rk[bi1 < S ? bi1 : 0];
+        vals[eb] = eb;
+      }
+    }
   }
 }
 
@@ -1671,8 +1788,11 @@ struct BatchCtx {
         BM_CHECK_CUDA(cudaMemcpyAsync(s_gel.ptr, gel.data(), gel.size() * 4,
                                       cudaMemcpyHostToDevice, stream));
         int32_t* d_order = s_rank.as<int32_t>() + nb_el * kGroupSeeds;
+        Scratch s_tab;
+        BM_TRY(scratch_alloc(s_tab, (size_t)nb_el * kSeedTab * 4, stream));
         seed_order_kernel<<<(unsigned)gel.size(), 256, 0, stream>>>(
-            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>(), d_order);
+            d_X, d, rows_b, d_offs, s_gel.as<int32_t>(), s_rank.as<int32_t>(), d_order,
+            s_tab.as<float>());
         BM_CHECK_LAUNCH();
         // seeds for the direction bound (fp32 copy, norms, pair distances;
         // direct: int8 seeds and their integer difference norms)
@@ -1695,9 +1815,14 @@ struct BatchCtx {
         BM_TRY(scratch_alloc(s_it, items.size() * sizeof(GroupItem), stream));
         BM_CHECK_CUDA(cudaMemcpyAsync(s_it.ptr, items.data(), items.size() * sizeof(GroupItem),
                                       cudaMemcpyHostToDevice, stream));
-        group_assign_kernel<<<(unsigned)items.size(), 128, 0, stream>>>(
-            d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_rank.as<int32_t>(),
-            s_k.as<uint64_t>(), s_v.as<int64_t>());
+        if (kGroupTc)
+          group_assign_tc_kernel<<<(unsigned)items.size(), kGaWarps * 32, 0, stream>>>(
+              d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_rank.as<int32_t>(),
+              s_tab.as<float>(), s_k.as<uint64_t>(), s_v.as<int64_t>());
+        else
+          group_assign_kernel<<<(unsigned)items.size(), 128, 0, stream>>>(
+              d_X, d, rows_b, d_offs, s_it.as<GroupItem>(), s_rank.as<int32_t>(),
+              s_tab.as<float>(), s_k.as<uint64_t>(), s_v.as<int64_t>());
         BM_CHECK_LAUNCH();
         int bits = 7;
         while (bits < 64 && ((uint64_t)nb_el << 7) >> bits) ++bits;

@@ -785,7 +785,10 @@ struct PruneBlock {
 };
 
 // flags[g] = 1 if dense tile pair g of the batch must be computed
-__global__ void __launch_bounds__(256)
+#ifndef BM_PRUNE_MINB
+#define BM_PRUNE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, BM_PRUNE_MINB)
 tile_prune_kernel(ElemTables et, int64_t d, const int32_t* __restrict__ tbase,
                   const PruneBlock* __restrict__ blocks, const double* __restrict__ cen,
                   const double* __restrict__ rad, double eps, double gamma,

@@ -266,12 +266,22 @@ void release_pool() {
 
 int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream) {
   retain_pool_once();
-  if (s.ptr) cudaFreeAsync(s.ptr, s.stream);
-  s.ptr = nullptr;
+  s.release();
   s.bytes = bytes;
   s.stream = stream;
   if (bytes == 0) bytes = 16;
+  // large scratch comes from the cached large buffers: growing the
+  // stream-ordered pool by GBs was measured to stall for 0.1-2.5 s when its
+  // reserve is fragmented (cfg5's windows)
+  if (bytes >= kScratchBig) return big_acquire(bytes, stream, &s.ptr, &s.slot);
+  static const bool trace_mem = getenv("B200MAP_TRACE_MEM") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMallocAsync(&s.ptr, bytes, stream);
+  if (trace_mem) {
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 1.0) fprintf(stderr, "[mem] scratch %.3f GB took %.1f ms\n", bytes / 1e9, ms);
+  }
   if (e != cudaSuccess) {  // idle cached large buffers hold the memory: free them, retry
     cudaGetLastError();
     if (getenv("B200MAP_TRACE_MEM"))

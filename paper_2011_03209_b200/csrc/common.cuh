@@ -81,23 +81,34 @@ void count_launch();
   } while (0)
 
 // Stream-ordered scratch buffer released on scope exit (cudaFreeAsync).
+void big_release(int slot, cudaStream_t stream);
+
 struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
   cudaStream_t stream = nullptr;
+  int slot = -1;  // >= 0: a cached large buffer (big_acquire), not the stream pool
   Scratch() = default;
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
   ~Scratch() { release(); }
   void release() {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (slot >= 0) {
+      big_release(slot, stream);
+    } else if (ptr) {
+      cudaFreeAsync(ptr, stream);
+    }
     ptr = nullptr;
+    slot = -1;
     bytes = 0;
   }
   template <typename T>
   T* as() const { return reinterpret_cast<T*>(ptr); }
 };
 
+// Stream-ordered scratch; at least kScratchBig bytes come from the cached
+// large buffers (big_acquire) instead of the stream-ordered pool.
+constexpr size_t kScratchBig = size_t(16) << 20;
 int scratch_alloc(Scratch& s, size_t bytes, cudaStream_t stream);
 
 // Stable sort of (keys, vals) by the low key_bits bits of keys (LSD radix,

@@ -216,6 +216,59 @@ __global__ void dense_edges_kernel(const int32_t* __restrict__ bins, int64_t n_n
   }
 }
 
+// Sort-free dense edges: every point lists the (few) nodes that hold it in
+// kSlots slots (one per cover element it lies in at most); the pairs of a
+// point's nodes are counted into the n_nodes^2 bins with warp-aggregated
+// atomics (few distinct edges). A point in more than kSlots nodes sets the
+// overflow flag and the caller takes the sorting path.
+constexpr int kSlots = 8;
+#ifndef BM_EDGE_SLOTS
+#define BM_EDGE_SLOTS 1
+#endif
+constexpr bool kEdgeSlots = BM_EDGE_SLOTS;
+
+__global__ void point_slots_kernel(const int64_t* __restrict__ node_rows,
+                                   const int64_t* __restrict__ node_off, int64_t n_nodes,
+                                   int64_t total, int32_t* __restrict__ cnt,
+                                   int32_t* __restrict__ slots, int32_t* __restrict__ overflow) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = n_nodes;
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (node_off[mid] <= i) a = mid; else b = mid;
+    }
+    const int64_t p = node_rows[i];
+    const int k = atomicAdd(cnt + p, 1);
+    if (k < kSlots) slots[p * kSlots + k] = (int32_t)a;
+    else *overflow = 1;
+  }
+}
+
+__global__ void point_pairs_kernel(const int32_t* __restrict__ cnt,
+                                   const int32_t* __restrict__ slots, int64_t n_points,
+                                   int64_t n_nodes, int32_t* __restrict__ bins) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_points;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = min(cnt[p], kSlots);
+    // the common case, one pair per point: warp-aggregated by bin
+    int64_t bin = -1;
+    if (c == 2) {
+      const int32_t u = slots[p * kSlots], v = slots[p * kSlots + 1];
+      bin = (int64_t)min(u, v) * n_nodes + max(u, v);
+    }
+    const unsigned act = __activemask();
+    const unsigned same = __match_any_sync(act, bin);
+    if (bin >= 0 && (__ffs(same) - 1) == (int)(threadIdx.x & 31)) atomicAdd(bins + bin, __popc(same));
+    if (c > 2)
+      for (int x = 0; x < c; ++x)
+        for (int y = x + 1; y < c; ++y) {
+          const int32_t u = slots[p * kSlots + x], v = slots[p * kSlots + y];
+          atomicAdd(bins + (int64_t)min(u, v) * n_nodes + max(u, v), 1);
+        }
+  }
+}
+
 __global__ void run_start_flags_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                        int32_t* __restrict__ flags) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -455,13 +508,18 @@ extern "C" int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_
   BM_CHECK_CUDA(cudaStreamSynchronize(s));
   if (total == 0) return BM_OK;
   Scratch kv;
-  BM_TRY(scratch_alloc(kv, total * 16 + 16, s));
-  uint64_t* keys = kv.as<uint64_t>();
-  int64_t* vals = (int64_t*)(keys + total);
-  entry_pairs_kernel<<<grid1(total), 256, 0, s>>>(d_node_rows, d_node_offsets, n_nodes, total,
-                                                  keys, vals);
-  BM_CHECK_LAUNCH();
-  BM_TRY(radix_sort_pairs(keys, vals, total, bits_for((uint64_t)std::max<int64_t>(n_points, 1)), s));
+  uint64_t* keys = nullptr;
+  int64_t* vals = nullptr;
+  auto sort_entries = [&]() -> int {  // (row, node) entries sorted by row
+    BM_TRY(scratch_alloc(kv, total * 16 + 16, s));
+    keys = kv.as<uint64_t>();
+    vals = (int64_t*)(keys + total);
+    entry_pairs_kernel<<<grid1(total), 256, 0, s>>>(d_node_rows, d_node_offsets, n_nodes, total,
+                                                    keys, vals);
+    BM_CHECK_LAUNCH();
+    return radix_sort_pairs(keys, vals, total,
+                            bits_for((uint64_t)std::max<int64_t>(n_points, 1)), s);
+  };
   const bool dense = n_nodes <= 4096;
   if (dense) {
     const int64_t nb = n_nodes * n_nodes;
@@ -470,9 +528,35 @@ extern "C" int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_
     BM_TRY(scratch_alloc(flags, nb * 4, s));
     BM_TRY(scratch_alloc(pos, (nb + 1) * 8, s));
     BM_CHECK_CUDA(cudaMemsetAsync(bins.ptr, 0, nb * 4, s));
-    run_pairs_dense_kernel<<<grid1(total), 256, 0, s>>>(keys, vals, total, n_nodes,
-                                                        bins.as<int32_t>());
-    BM_CHECK_LAUNCH();
+    bool sorted_path = !kEdgeSlots;
+    if (kEdgeSlots) {
+      Scratch sc;
+      BM_TRY(scratch_alloc(sc, (size_t)n_points * 4 * (1 + kSlots) + 16, s));
+      int32_t* cnt = sc.as<int32_t>();
+      int32_t* slots = cnt + n_points;
+      int32_t* ovf = slots + n_points * kSlots;
+      BM_CHECK_CUDA(cudaMemsetAsync(cnt, 0, n_points * 4, s));
+      BM_CHECK_CUDA(cudaMemsetAsync(ovf, 0, 4, s));
+      point_slots_kernel<<<grid1(total), 256, 0, s>>>(d_node_rows, d_node_offsets, n_nodes, total,
+                                                      cnt, slots, ovf);
+      BM_CHECK_LAUNCH();
+      int32_t h_ovf = 0;
+      BM_CHECK_CUDA(cudaMemcpyAsync(&h_ovf, ovf, 4, cudaMemcpyDeviceToHost, s));
+      BM_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (h_ovf) {
+        sorted_path = true;
+      } else {
+        point_pairs_kernel<<<grid1(n_points), 256, 0, s>>>(cnt, slots, n_points, n_nodes,
+                                                           bins.as<int32_t>());
+        BM_CHECK_LAUNCH();
+      }
+    }
+    if (sorted_path) {
+      BM_TRY(sort_entries());
+      run_pairs_dense_kernel<<<grid1(total), 256, 0, s>>>(keys, vals, total, n_nodes,
+                                                          bins.as<int32_t>());
+      BM_CHECK_LAUNCH();
+    }
     nonzero_flags_kernel<<<grid1(nb), 256, 0, s>>>(bins.as<int32_t>(), nb, flags.as<int32_t>());
     BM_CHECK_LAUNCH();
     BM_TRY(exclusive_scan_i32_to_i64(flags.as<int32_t>(), pos.as<int64_t>(), nb, s));
@@ -492,6 +576,7 @@ extern "C" int bm_nerve_edges(const int64_t* d_node_rows, const int64_t* d_node_
     return BM_OK;
   }
   // sparse: materialise pair keys, sort, run-length encode
+  BM_TRY(sort_entries());
   Scratch np, pk, fl, ps;
   BM_TRY(scratch_alloc(np, (total + 1) * 8, s));
   run_pairs_count_kernel<<<grid1(total), 256, 0, s>>>(keys, total, np.as<int64_t>());

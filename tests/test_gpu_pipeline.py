@@ -139,3 +139,31 @@ def test_nerve_edges_sparse_path_matches_oracle():
                                n_nodes, n_points)
     want = O.nerve_edges_fast([r.tolist() for r in node_rows], n_points)
     assert [tuple(e) for e in edges.tolist()] == want
+
+
+@pytest.mark.parametrize("max_nodes_per_point", [2, 4, 8, 9, 30])
+def test_nerve_edges_dense_slots_and_overflow(max_nodes_per_point):
+    """Dense path (<= 4096 nodes): points in <= 8 nodes take the sort-free
+    slot path; a point in more nodes sends the call down the sorting path.
+    Both equal the oracle's nerve edges."""
+    import torch
+
+    from paper_2011_03209_b200 import engine
+    from paper_2011_03209_b200.device import require_gpu
+
+    dev = require_gpu()
+    rng = np.random.default_rng(max_nodes_per_point)
+    n_points, n_nodes = 30_000, 300
+    member = [[] for _ in range(n_nodes)]
+    for p in range(n_points):
+        k = int(rng.integers(1, max_nodes_per_point + 1)) if p % 7 == 0 else int(rng.integers(1, 3))
+        for v in rng.choice(n_nodes, min(k, max_nodes_per_point), replace=False):
+            member[v].append(p)
+    node_rows = [np.array(sorted(m), dtype=np.int64) for m in member if m]
+    off = np.zeros(len(node_rows) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in node_rows], out=off[1:])
+    flat = np.concatenate(node_rows)
+    edges = engine.nerve_edges(torch.from_numpy(flat).to(dev), torch.from_numpy(off).to(dev),
+                               len(node_rows), n_points)
+    want = O.nerve_edges_fast([r.tolist() for r in node_rows], n_points)
+    assert [tuple(e) for e in edges.tolist()] == want

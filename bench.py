@@ -83,29 +83,40 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
+    PERIOD_MS = 20
+
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: the timed region begins once
+            # it samples, so even a short region is covered
+            deadline = time.perf_counter() + 10.0
+            while not self.lines and time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *exc):
+        self.t1 = time.perf_counter()
         if self.proc:
+            time.sleep(2.5 * self.PERIOD_MS / 1e3)  # the sample that spans the region's end
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -115,7 +126,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples that arrived during the timed region (+ one period after it)
+        t1 = (self.t1 or time.perf_counter()) + 1.5 * self.PERIOD_MS / 1e3
+        inside = [ln for t, ln in self.lines if self.t0 is not None and self.t0 <= t <= t1]
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -128,7 +142,8 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "region_s": None if self.t0 is None or self.t1 is None else self.t1 - self.t0}
 
 
 def alg_flops(sizes, d):
@@ -136,7 +151,7 @@ def alg_flops(sizes, d):
     return float((2.0 * d * s * (s - 1) / 2.0).sum())
 
 
-TRAFFIC_PROFILE = "profiles/r02_ncu_full_cfg3.txt"
+TRAFFIC_PROFILE = "profiles/r02d_ncu_full_cfg3.txt"
 
 
 def ncu_traffic(kernel="tc_adjacency_kernel"):

@@ -934,8 +934,10 @@ __device__ __forceinline__ QRow quantize_row(const double* __restrict__ xr,
   const bool redo = ((__ballot_sync(0xffffffffu, bad) >> (16 * half)) & 0xffffu) != 0;
   if (redo) nsum = 0, msq = lsq = 0, esum = ysum = rsum = 0.0;
   // generic path: the tail columns (or the whole row when redo / padding);
-  // the fast path covered whole 64-column blocks (vec) or 4-column groups
-  for (int64_t c4 = 4 * hl; c4 < kpad; c4 += 64) {
+  // the fast path covered whole 64-column blocks (vec) or 4-column groups,
+  // so a fast row starts after its last whole 64-column block
+  const int64_t g0 = (!redo && valid) ? (d / 64) * 64 : 0;
+  for (int64_t c4 = g0 + 4 * hl; c4 < kpad; c4 += 64) {
     if (!redo && valid && (vec ? (c4 - c4 % 64) + 64 <= d : c4 + 4 <= d)) continue;
     uint32_t hw = 0, mw = 0, lw = 0;
 #pragma unroll
@@ -1212,6 +1214,7 @@ quantize_rows_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, i
     }
     const int k = (int)a;  // tiles never straddle elements
     const double sc = scale[k], inv = 1.0 / sc;
+    const int64_t p_end = et.pbase[k] + et.nrows[k];  // first pad row of the element
     __syncthreads();  // the previous tile's readers of s_c / s_red are done
     for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
       s_c[c] = center[(int64_t)k * d + c];
@@ -1225,7 +1228,7 @@ quantize_rows_kernel(const RowSrc src, int64_t d, int64_t kpad, ElemTables et, i
       const int64_t p = tile * kTile + warp * (2 * kIt) + j * 2 + half;
       BM_DASSERT(p < P);
       mbar_wait(&wbar[warp][slot], phase);
-      const bool valid = (p - et.pbase[k]) < et.nrows[k];
+      const bool valid = p < p_end;
       const QRow qr = quantize_row(ring + (slot * 2 + half) * d, s_c, cen ? s_c + d : nullptr,
                                    valid, d, kpad, sc, inv, planes + p * kpad,
                                    planes + P * kpad + p * kpad, planes + 2 * P * kpad + p * kpad,

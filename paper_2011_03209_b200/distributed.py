@@ -278,7 +278,7 @@ def build_distributed(X, pc, params, rank: int, world: int, dist, budget_bytes=N
     if F is None:  # else: the caller's (N, m) device lens (FilterValues)
         cols = [evaluate_device(X, pc, s) for s in params.filters]
         F = torch.stack(cols, dim=1).contiguous() if len(cols) > 1 else cols[0].reshape(-1, 1)
-    rng = torch.stack([F.amin(dim=0), F.amax(dim=0)], dim=1).cpu().numpy()
+    rng = torch.stack(torch.aminmax(F, dim=0), dim=1).cpu().numpy()
     cover = build_cover_from_range([(rng[a, 0], rng[a, 1]) for a in range(F.shape[1])],
                                    params.n, params.p)
     rows, offsets = eng.membership(F, cover)

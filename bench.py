@@ -458,20 +458,70 @@ def subsystem_roofline(w, g, st, params):
     return out
 
 
-def library_pieces(Xnp, Fnp, w, params):
-    """cfg4's reference-facing path: the library pieces on host inputs."""
+def library_pieces(Xnp, Fnp, w, params, marks=None):
+    """cfg4's reference-facing path: the library pieces on host inputs.
+    marks: optional callable(name) after each piece (phase timing)."""
     from paper_2011_03209_b200 import (DbscanParams, FilterValues, build_cover, build_graph,
                                        cluster_all, from_array, graph_to_json, membership)
 
+    mark = marks or (lambda name: None)
     pc = from_array(Xnp)
     fv = FilterValues(values=Fnp, specs=list(params.filters))
     cover = build_cover(fv, list(w.intervals), list(w.overlaps))
+    mark("cover")
     members = membership(fv, cover)
+    mark("membership (lens upload + binning)")
     cl = cluster_all(pc, members, DbscanParams(w.eps, w.min_pts), params.strategy,
                      budget_bytes=BUDGET)
+    mark("cluster_all (X upload + DBSCAN)")
     g = build_graph(cl, pc, fv, cover, manifest=params.manifest())
+    mark("build_graph (edges + payload)")
     graph_to_json(g)
+    mark("json")
     return g
+
+
+def e2e_phases(Xnp, Fnp, w, params, engine, dev):
+    """One extra, untimed-for-`e2e` run of the end-to-end path with a device
+    synchronisation after each phase (H2D of X and node stats +
+    JSON reported separately). Milliseconds per phase."""
+    import torch
+
+    from paper_2011_03209_b200 import engine as eng
+    from paper_2011_03209_b200 import from_array, nerve as NV, pipeline as PL
+    from paper_2011_03209_b200.device import to_device_f64
+
+    T = {}
+    t = [time.perf_counter()]
+
+    def mark(name):
+        torch.cuda.synchronize(dev)
+        now = time.perf_counter()
+        T[name] = round((now - t[0]) * 1e3, 3)
+        t[0] = now
+
+    if Fnp is not None:
+        library_pieces(Xnp, Fnp, w, params, marks=mark)
+        return T
+    pc = from_array(Xnp)
+    Xd = to_device_f64(pc.points, dev)
+    mark("h2d X")
+    Xn = eng.normalize(Xd, params.norm)
+    g = PL.build_device(Xn, pc, params, BUDGET, None, engine)
+    mark("build (lens, cover, DBSCAN, nodes, edges)")
+    st, fm = eng.node_payload(Xn, g.F, g.node_rows, g.node_off, g.n_nodes)
+    mark("node payload (stats, filter means)")
+    host = [PL._pinned_copy(x) for x in (g.node_rows, g.node_off, st, fm)]
+    mark("d2h")
+    rows_np, off_np, st_np, fm_np = (h.numpy() for h in host)
+    manifest = params.manifest()
+    manifest["intervals"] = [[[iv.lo, iv.hi] for iv in axis] for axis in g.cover.axes]
+    graph = NV.assemble_graph(pc, None, g.cover, manifest, rows_np, off_np, g.node_elem, st_np,
+                              fm_np, g.edges)
+    mark("graph objects")
+    NV.graph_to_json(graph)
+    mark("canonical json")
+    return T
 
 
 def config_of(w, world):
@@ -596,6 +646,7 @@ def main():
     h2d = X.nbytes
     d2h = 0
     e2e_pageable = None
+    phases = None
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     if world == 1:
@@ -639,6 +690,8 @@ def main():
         e2e_pageable = {"value": w.n * n_page / t_page, "unit": UNIT,
                         "ms_per_step": 1e3 * t_page / n_page, "steps": n_page,
                         "source": "pageable numpy arrays (staged through the pinned ring)"}
+        phases = e2e_phases(Xh.numpy(), None if Fh is None else Fh.numpy(), w, params,
+                            args.engine, dev)
         n_rows = sum(len(nd.rows) for nd in gr.nodes)
         d2h = 8 * (n_rows + gr.n_nodes + 1 + gr.n_nodes * (w.d + len(params.filters)) +
                    3 * len(gr.edges))
@@ -697,7 +750,9 @@ def main():
         "data": "synthetic", "config": config_of(w, world),
         "e2e": {"value": w.n * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t_e2e / args.steps,
-                "api": e2e_api, "pageable": e2e_pageable},
+                "api": e2e_api, "pageable": e2e_pageable,
+                "phases_ms": phases, "phases_note": "one extra run, synchronised after each "
+                                                    "phase (page-locked host inputs)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(),
                      "traffic_note": "DRAM bytes per tc_adjacency_kernel launch at cfg3, from "

@@ -76,7 +76,8 @@ def _copy_pool():
     if _POOL is None:
         from concurrent.futures import ThreadPoolExecutor
 
-        _POOL = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1),
+        n = int(os.environ.get("B200MAP_STAGE_THREADS", "16"))
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(n, os.cpu_count() or 1)),
                                    thread_name_prefix="b200map-stage")
     return _POOL
 

@@ -1637,12 +1637,15 @@ colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ no
     if (tr.I == tr.J) continue;
     const uint4* b = reinterpret_cast<const uint4*>(adj + s * kTileWords);
     uint4 r[4];
-#pragma unroll
-    for (int rb = 0; rb < 4; ++rb) r[rb] = b[rb * 32 + lane];
     if (cand) {
-      // candidate columns only: one ballot per 32-row block and column
+      // candidate columns only: one ballot per 32-row block and column; a
+      // tile without candidate columns is not even read (most of them: rows
+      // reach min_pts from their row counts alone)
       const int64_t pj = et.pbase[tr.k] + tr.J * kTile;
       const uint4 cm = *reinterpret_cast<const uint4*>(cand + (pj >> 5));
+      if ((cm.x | cm.y | cm.z | cm.w) == 0u) continue;  // warp-uniform
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) r[rb] = b[rb * 32 + lane];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t m = w == 0 ? cm.x : w == 1 ? cm.y : w == 2 ? cm.z : cm.w;
@@ -1660,6 +1663,8 @@ colcount_kernel(const uint32_t* __restrict__ adj, const int32_t* __restrict__ no
       }
       continue;
     }
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) r[rb] = b[rb * 32 + lane];
     const int64_t base = et.pbase[tr.k] + tr.J * kTile + lane;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {

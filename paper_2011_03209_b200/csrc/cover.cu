@@ -55,13 +55,25 @@ __device__ __forceinline__ void axis_range(const double* lo, const double* hi, i
 }
 
 // PASS 1 (COUNT=true) / PASS 2 (COUNT=false): one warp per chunk of rows.
-template <bool COUNT>
+// SMEM: the warp keeps its chunk's cursors of all n_el elements in shared
+// memory (loaded once, written back once) instead of a global load/store per
+// served element.
+constexpr int kSmemEl = 256;  // largest element count with shared-memory cursors
+
+template <bool COUNT, bool SMEM>
 __global__ void membership_kernel(const double* __restrict__ f, int64_t n, AxisTable t,
                                   int64_t n_chunks, int64_t* __restrict__ cursor,
                                   int64_t* __restrict__ rows_out) {
+  extern __shared__ int64_t s_cur[];
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (chunk >= n_chunks) return;
+  const int n_el = t.n0 * t.n1;
+  int64_t* const wc = SMEM ? s_cur + (threadIdx.x >> 5) * (int64_t)n_el : nullptr;
+  if (SMEM) {
+    for (int k = lane; k < n_el; k += 32) wc[k] = cursor[(int64_t)k * n_chunks + chunk];
+    __syncwarp();
+  }
   const int64_t r0 = chunk * kChunk;
   const int64_t r1 = min(n, r0 + kChunk);
   const unsigned lt = (1u << lane) - 1u;
@@ -91,7 +103,7 @@ __global__ void membership_kernel(const double* __restrict__ f, int64_t n, AxisT
       const bool mine = key == kmin;
       const unsigned peers = __ballot_sync(0xffffffffu, mine);
       const int leader = __ffs(peers) - 1;
-      int64_t* cur = &cursor[(int64_t)kmin * n_chunks + chunk];
+      int64_t* cur = SMEM ? &wc[kmin] : &cursor[(int64_t)kmin * n_chunks + chunk];
       int64_t basepos = 0;
       if (lane == leader) basepos = *cur;
       basepos = __shfl_sync(0xffffffffu, basepos, leader);
@@ -103,6 +115,22 @@ __global__ void membership_kernel(const double* __restrict__ f, int64_t n, AxisT
       __syncwarp();
     }
   }
+  if (SMEM && COUNT)
+    for (int k = lane; k < n_el; k += 32) cursor[(int64_t)k * n_chunks + chunk] = wc[k];
+}
+
+template <bool COUNT>
+void launch_membership(const double* f, int64_t n, const AxisTable& t, int64_t n_chunks,
+                       int64_t* cursor, int64_t* rows_out, cudaStream_t stream) {
+  const int warps = 4;
+  const unsigned blocks = (unsigned)ceil_div(n_chunks, warps);
+  const int64_t n_el = (int64_t)t.n0 * t.n1;
+  if (n_el <= kSmemEl)
+    membership_kernel<COUNT, true><<<blocks, warps * 32, warps * n_el * sizeof(int64_t), stream>>>(
+        f, n, t, n_chunks, cursor, rows_out);
+  else
+    membership_kernel<COUNT, false><<<blocks, warps * 32, 0, stream>>>(f, n, t, n_chunks, cursor,
+                                                                      rows_out);
 }
 
 // counts[k] = sum over chunks of C[k][chunk]
@@ -170,10 +198,7 @@ int count_table(const double* f, int64_t n, Prepared& p, Scratch& C, cudaStream_
   BM_TRY(scratch_alloc(C, (cells + 1) * sizeof(int64_t), stream));
   BM_CHECK_CUDA(cudaMemsetAsync(C.ptr, 0, (cells + 1) * sizeof(int64_t), stream));
   if (n == 0) return BM_OK;
-  const int warps = 4;
-  unsigned blocks = (unsigned)ceil_div(p.n_chunks, warps);
-  membership_kernel<true><<<blocks, warps * 32, 0, stream>>>(f, n, p.t, p.n_chunks,
-                                                              C.as<int64_t>(), nullptr);
+  launch_membership<true>(f, n, p.t, p.n_chunks, C.as<int64_t>(), nullptr, stream);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }
@@ -230,9 +255,7 @@ extern "C" int bm_membership_fill(const double* d_f, int64_t n, int m, const dou
   add_offsets_kernel<<<(unsigned)ceil_div(cells, 256), 256, 0, stream>>>(
       C.as<int64_t>(), p.n_chunks, p.n_el, d_offsets, first.as<int64_t>());
   BM_CHECK_LAUNCH();
-  const int warps = 4;
-  membership_kernel<false><<<(unsigned)ceil_div(p.n_chunks, warps), warps * 32, 0, stream>>>(
-      d_f, n, p.t, p.n_chunks, C.as<int64_t>(), d_rows);
+  launch_membership<false>(d_f, n, p.t, p.n_chunks, C.as<int64_t>(), d_rows, stream);
   BM_CHECK_LAUNCH();
   return BM_OK;
 }

@@ -115,6 +115,16 @@ def test_membership_matches_oracle_2d(dev, seed):
     assert got == want
 
 
+@pytest.mark.parametrize("n", [[300], [20, 25], [16, 16], [17, 16]])
+def test_membership_many_elements(dev, n):
+    """Element counts around and above the shared-memory cursor limit (256)."""
+    rng = np.random.default_rng(sum(n))
+    m = len(n)
+    v = rng.standard_normal((40_000, m)) if m == 2 else rng.standard_normal(40_000)
+    got, want = _gpu_membership(v, n, [0.4] * m, dev)
+    assert got == want
+
+
 def test_membership_boundary_and_degenerate(dev):
     got, want = _gpu_membership([0.0, 0.5, 1.0], [2], [0.0], dev)  # test_cover.py:56-61
     assert got == [[0, 1], [1, 2]] == want

@@ -11,8 +11,10 @@
  *     host memory owned by the caller.  The library never returns memory the
  *     caller must free; internal scratch is stream-ordered (cudaMallocAsync)
  *     and freed before the call returns, but the device's default pool keeps
- *     it mapped for the next call (bm_release_scratch trims it;
- *     B200MAP_POOL_RELEASE=1 disables the retention).
+ *     it mapped for the next call, and scratch of 16 MB and more (bitmaps,
+ *     limb planes, tile tables) stays in a per-device cache of large
+ *     buffers that later calls reuse (bm_release_scratch frees both;
+ *     B200MAP_POOL_RELEASE=1 disables the pool retention).
  *   - `stream` is a cudaStream_t (passed as void*); NULL = legacy stream.
  *     Calls that must size outputs synchronise that stream.
  *   - Return value: 0 on success, BM_ERR_DATA (-1) for invalid arguments

@@ -177,9 +177,15 @@ def cached_device_array(owner, arr: np.ndarray, dev):
 
 
 def release_device_cache() -> None:
-    """Drop every cached device copy (frees their HBM)."""
+    """Drop every cached device copy and give the library's cached scratch
+    (large buffers and the stream-ordered pool's reserve) back to the device,
+    e.g. before handing the GPU to other work."""
     with _DEV_CACHE_LOCK:
         _DEV_CACHE.clear()
+    from . import _native
+
+    lib = _native.load()
+    _native.check(lib.bm_release_scratch(), "release scratch")
 
 
 def to_device_i64(arr: np.ndarray, dev):

@@ -81,3 +81,21 @@ def test_library_pieces_upload_points_once(monkeypatch):
     # a new object with the same contents uploads again
     cluster_all(from_array(X), members, DbscanParams(eps, 5), DistanceStrategy())
     assert calls.count(X.shape) == 2
+
+
+def test_release_device_cache_then_rebuild(golden):
+    """release_device_cache() drops the device copies and the library's cached
+    scratch (large buffers + pool reserve); the next build allocates again and
+    still gives the reference's bytes."""
+    import torch
+
+    import cases
+    from paper_2011_03209_b200 import device
+    from test_gpu_pipeline import graph_bytes
+
+    X, p = cases.cfg1()
+    z = golden("cfg1")
+    assert graph_bytes(X, p, 0) == z["graph"].tobytes()
+    torch.cuda.synchronize()
+    device.release_device_cache()
+    assert graph_bytes(X, p, 0) == z["graph"].tobytes()

@@ -1222,6 +1222,11 @@ __device__ unsigned long long g_comp_stats[8];
 
 // off-diagonal phases: tile pairs [kCompCuts[i-1], kCompCuts[i]) of every unit,
 // with a compression of the forest between phases
+#ifndef BM_DIAG_BFS
+#define BM_DIAG_BFS 1
+#endif
+constexpr bool kDiagBfs = BM_DIAG_BFS;  // diagonal pass: mask BFS (diag_bfs_kernel)
+
 #ifndef BM_COMP_CUT1
 #define BM_COMP_CUT1 6
 #endif
@@ -1443,6 +1448,109 @@ components_kernel(const uint32_t* __restrict__ adj, ElemTables et,
         }
         if (ci) gr = uf_find(par, gr);  // refresh the row roots after merges
       }
+    }
+  }
+}
+
+// Diagonal pass as a breadth-first search over 128-bit masks. Each row is in
+// exactly one diagonal tile, so a tile's components are found inside its CTA
+// and every core row is joined to its component's smallest row by one union
+// (uncontended: each row hooks its own root). Per component, each
+// BFS level ORs the bitmap rows of the frontier with one block reduction;
+// a dense tile is one component found in 2-3 levels instead of a walk over
+// its ~8k bits. Isolated core rows are settled before the search.
+__global__ void __launch_bounds__(128)
+diag_bfs_kernel(const uint32_t* __restrict__ adj, ElemTables et,
+                const TileUnit* __restrict__ units, const TileRef* __restrict__ tiles,
+                int64_t slot0, int64_t n_units, const uint8_t* __restrict__ core,
+                int32_t* __restrict__ par, int32_t* __restrict__ bmin) {
+  __shared__ uint32_t s_core[4];
+  __shared__ uint32_t s_red[4][4];
+  __shared__ uint32_t s_rem[4];
+  const int t = threadIdx.x, lane = t & 31, wq = t >> 5;
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const TileUnit un = units[u];
+    const int k = un.k, I = un.I;
+    const int64_t g = un.off;  // the row tile's first kept tile: its diagonal
+    BM_DASSERT(tiles[g].k == k && tiles[g].I == I && tiles[g].J == I);
+    const int64_t pb = et.pbase[k];
+    const int nk = et.nrows[k];
+    const int pI = (int)(pb + I * kTile);
+    const uint4 rw = reinterpret_cast<const uint4*>(adj + (g - slot0) * kTileWords)[t];
+    const bool ci = core[pI + t];
+    __syncthreads();  // the previous unit's readers of s_core / s_rem are done
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, ci);
+      if (lane == 0) s_core[wq] = b;
+    }
+    __syncthreads();
+    const uint32_t c0 = s_core[0], c1 = s_core[1], c2 = s_core[2], c3 = s_core[3];
+    // my row's core neighbours other than myself
+    uint32_t nb[4] = {rw.x & c0, rw.y & c1, rw.z & c2, rw.w & c3};
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      if (w == wq) nb[w] &= ~(1u << lane);  // static indices: no local memory
+    const bool lonely = ci && !(nb[0] | nb[1] | nb[2] | nb[3]);
+    int lab = ci ? t : -1;  // component's smallest row (lonely rows: themselves)
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, ci && !lonely);
+      if (lane == 0) s_rem[wq] = b;
+    }
+    __syncthreads();
+    uint32_t rem[4] = {s_rem[0], s_rem[1], s_rem[2], s_rem[3]};  // block-uniform
+    while (rem[0] | rem[1] | rem[2] | rem[3]) {
+      const int wseed = rem[0] ? 0 : rem[1] ? 1 : rem[2] ? 2 : 3;
+      const uint32_t rs = rem[0] ? rem[0] : rem[1] ? rem[1] : rem[2] ? rem[2] : rem[3];
+      const int seed = wseed * 32 + __ffs(rs) - 1;
+      uint32_t comp[4], front[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) comp[w] = front[w] = w == wseed ? 1u << (seed & 31) : 0u;
+      while (true) {
+        const uint32_t fw = wq == 0 ? front[0] : wq == 1 ? front[1] : wq == 2 ? front[2] : front[3];
+        const bool in_front = (fw >> lane) & 1u;
+        uint32_t m[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) m[w] = in_front ? nb[w] : 0u;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) m[w] = __reduce_or_sync(0xffffffffu, m[w]);
+        if (lane == 0) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w) s_red[wq][w] = m[w];
+        }
+        __syncthreads();
+        uint32_t any = 0u;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t all = s_red[0][w] | s_red[1][w] | s_red[2][w] | s_red[3][w];
+          front[w] = all & ~comp[w];
+          comp[w] |= front[w];
+          any |= front[w];
+        }
+        __syncthreads();  // s_red is rewritten by the next level
+        if (!any) break;  // block-uniform
+      }
+      const uint32_t cwq = wq == 0 ? comp[0] : wq == 1 ? comp[1] : wq == 2 ? comp[2] : comp[3];
+      if ((cwq >> lane) & 1u) lab = seed;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) rem[w] &= ~comp[w];
+    }
+    if (ci) {
+      // a union, not a store: in row windows (huge elements) an earlier
+      // window's off-diagonal pass may already have hooked these rows
+      if (lab != t) uf_union(par, pI + t, pI + lab);
+    } else if (t < nk - I * kTile) {
+      // border: non-core row -> its core neighbour of smallest ENTRY
+      int best = kNoCore;
+      const uint32_t cw[4] = {rw.x & c0, rw.y & c1, rw.z & c2, rw.w & c3};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = cw[w];
+        while (m) {
+          best = min(best, et.ent[pI + w * 32 + __ffs(m) - 1]);
+          m &= m - 1;
+        }
+      }
+      if (best < __ldcg(bmin + pI + t)) atomicMin(bmin + pI + t, best);
     }
   }
 }
@@ -2091,9 +2199,13 @@ struct BatchCtx {
       BM_REQUIRE_INTERNAL(h_bad == 0, "asymmetric diagonal tile bitmap (%llu bits)", h_bad);
     }
     if (w.n_diag > 0) {
-      components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
-          adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty, 0,
-          1 << 30);
+      if (kDiagBfs)
+        diag_bfs_kernel<<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
+            adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w);
+      else
+        components_kernel<true><<<grid_for(w.n_diag, 1, 32), 128, 0, stream>>>(
+            adj, et, w.diag, w.tiles, w.slot0, w.n_diag, core, par_w, bmin_w, nullptr, nonempty, 0,
+            1 << 30);
       BM_CHECK_LAUNCH();
     }
     compress_kernel<<<grid_for(P, 256), 256, 0, stream>>>(par_w, core, P);

@@ -125,6 +125,11 @@ __device__ __forceinline__ void stat_acc(double v, double& mn, double& mx, doubl
   sm += v;
 }
 
+#ifndef BM_STAT_ROWS
+#define BM_STAT_ROWS 4
+#endif
+constexpr int kStatRows = BM_STAT_ROWS;  // row loads in flight per thread
+
 __global__ void __launch_bounds__(128)
 tile_stats_kernel(const double* __restrict__ X, int64_t d, const int64_t* __restrict__ xrow,
                   double* __restrict__ tmin, double* __restrict__ tmax,
@@ -139,13 +144,13 @@ tile_stats_kernel(const double* __restrict__ X, int64_t d, const int64_t* __rest
   for (int64_t c = 2 * threadIdx.x; c < d; c += 2 * blockDim.x) {
     double mn0 = inf, mx0 = -inf, sm0 = 0.0, mn1 = inf, mx1 = -inf, sm1 = 0.0;
     int r = 0;
-    for (; r + 8 <= valid; r += 8) {
-      double2 v[8];
+    for (; r + kStatRows <= valid; r += kStatRows) {
+      double2 v[kStatRows];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < kStatRows; ++u)
         v[u] = __ldg(reinterpret_cast<const double2*>(X + src[r + u] * d + c));
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kStatRows; ++u) {
         stat_acc(v[u].x, mn0, mx0, sm0);
         stat_acc(v[u].y, mn1, mx1, sm1);
       }

@@ -151,7 +151,7 @@ def alg_flops(sizes, d):
     return float((2.0 * d * s * (s - 1) / 2.0).sum())
 
 
-TRAFFIC_PROFILE = "profiles/r02e_ncu_full_cfg3.txt"
+TRAFFIC_PROFILE = "profiles/r02f_ncu_full_cfg3.txt"
 
 
 def ncu_traffic(kernel="tc_adjacency_kernel"):
